@@ -1,0 +1,313 @@
+// ============================================================================================
+//  CacheSolidarity ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+//  A plain, slow, sequential CPU implementation of what the hot path computes:
+//  a dict-based prefix cache (std::unordered_map) plus the per-request selective-isolation state
+//  machine of PAPER.md "System Design > KV Cache Extension and Detector".
+//
+//  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+//  load this library.  It shares NO code, header, table or constant generator with the CUDA path
+//  (paper_2603_10726_b200/csrc); both implement DESIGN.md §2 (semantics) independently.
+//
+//  Requests are processed strictly one at a time in global sequence order (reading R1:
+//  sequential semantics).  There is no notion of a batch here.
+//
+//  Pins (tests/test_oracle_*.py): worked example t1-t4 (golden/p1_example.json),
+//  attacker experiment (golden/p2_attack.json), the §5 guarantee by brute force
+//  (P:560-603), APC == brute-force longest common prefix, user isolation == per-user LCP,
+//  enforce=0 == APC, an independent content-keyed trie reference, splitmix64 published vector,
+//  and the chain value against a closed-form big-integer polynomial.
+//  "parity unpinned": fmix64 outputs (an arbitrary finaliser; pinned only by bijectivity and by
+//  agreement with the independent CUDA implementation).
+// ============================================================================================
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+typedef unsigned __int128 u128;
+
+// ---- DESIGN.md §2.1 "H-def v2" (the paper is silent on hashing, P:937 is the only "hash") ----
+const uint64_t P61 = (1ULL << 61) - 1;            // p = 2^61 - 1
+const uint64_t NONE = 0xFFFFFFFFULL;              // "no user" (sharer unset)
+const uint64_t KEY_OFFSET = 0x9E3779B97F4A7C15ULL; // key = fmix64(S + KEY_OFFSET)
+const uint64_t SIGMA_SALT = 0xD1B54A32D192ED03ULL;
+
+uint64_t mulmod(uint64_t a, uint64_t b) { return (uint64_t)(((u128)a * (u128)b) % P61); }
+uint64_t addmod(uint64_t a, uint64_t b) { return (uint64_t)(((u128)a + (u128)b) % P61); }
+
+// splitmix64 (Vigna): one output for state x (the generator adds the golden gamma first).
+uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// MurmurHash3 64-bit finaliser.
+uint64_t fmix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+
+uint64_t key_of(uint64_t S) {
+  uint64_t k = fmix64(S + KEY_OFFSET);
+  return k == 0 ? 1 : k;   // never taken (S < 2^61 keeps S+offset away from 0); kept per H-def
+}
+
+struct Entry {
+  uint32_t owner;    // OwnerID: set exactly once at allocation
+  uint32_t sharer;   // user that flagged the entry; AttackFlag <=> sharer != NONE (R5)
+};
+
+struct Ctx {
+  uint32_t bs;
+  uint64_t seed;
+  int policy;        // 0 = APC, 1 = USER_ISOLATION, 2 = SOLIDARITY
+  uint64_t B, M;
+  std::vector<uint64_t> K;   // K_i = B^i mod p
+  std::unordered_map<uint64_t, Entry> table;
+  uint64_t next_seq;
+};
+
+uint64_t sigma_of(const Ctx& c, uint32_t user) {
+  // sigma(Iso(u)) = 1 + (splitmix64(seed ^ SALT ^ u) mod (p - 1))   in [1, p-1]
+  return 1 + splitmix64(c.seed ^ SIGMA_SALT ^ (uint64_t)user) % (P61 - 1);
+}
+
+// h(block) = sum_i x_i * K_i mod p, x_i = token_i + 1
+uint64_t block_hash(const Ctx& c, const uint32_t* tok) {
+  uint64_t h = 0;
+  for (uint32_t i = 0; i < c.bs; ++i) h = addmod(h, mulmod((uint64_t)tok[i] + 1, c.K[i]));
+  return h;
+}
+
+// One chain step (SPEC chain_hash(parent, block, ns), with the block's depth b made
+// explicit):  S[b] = S[b-1] + M^(b-1) * (h_b + sigma_ns)  (mod p).
+uint64_t chain_step(uint64_t parent, uint64_t Mpow_bm1, uint64_t h, uint64_t sigma) {
+  return addmod(parent, mulmod(Mpow_bm1, addmod(h, sigma)));
+}
+
+bool present(const Ctx& c, uint64_t key) { return c.table.count(key) != 0; }
+bool flagged(const Ctx& c, uint64_t key) { return c.table.at(key).sharer != NONE; }
+uint32_t owner_of(const Ctx& c, uint64_t key) { return c.table.at(key).owner; }
+
+// "On a cache miss, a new cache entry is created and tagged with the user's ID".
+// Inserting a key that is already present leaves it unchanged (R8).
+void insert_if_absent(Ctx& c, uint64_t key, uint32_t user) {
+  if (!present(c, key)) c.table.emplace(key, Entry{user, (uint32_t)NONE});
+}
+
+}  // namespace
+
+extern "C" {
+
+struct oracle_result {        // same field meaning as DESIGN.md §2.4 (24 bytes)
+  uint32_t n_blocks;          // floor(len / bs)
+  uint32_t shared_hits;       // k
+  uint32_t reused;            // r
+  int32_t divert_at;          // f or -1
+  uint32_t flag_depth;        // depth of the entry this request flagged, 0 = none
+  uint32_t bits;              // HIT=1 FULL=2 DIVERTED=4 TRUNCATED=8 FLAGGED=16
+};
+
+struct oracle_entry {
+  uint64_t key;
+  uint32_t owner;
+  uint32_t sharer;
+};
+
+void* oracle_create(uint32_t block_size, uint64_t seed, int policy) {
+  if (block_size == 0 || policy < 0 || policy > 2) return nullptr;
+  Ctx* c = new Ctx();
+  c->bs = block_size;
+  c->seed = seed;
+  c->policy = policy;
+  // B = 2^32 + (splitmix64(seed) mod (p - 2^33))
+  c->B = (1ULL << 32) + splitmix64(seed) % (P61 - (1ULL << 33));
+  c->K.resize(block_size);
+  uint64_t pw = 1;
+  for (uint32_t i = 0; i < block_size; ++i) { c->K[i] = pw; pw = mulmod(pw, c->B); }
+  c->M = pw;                  // M = B^bs
+  c->next_seq = 0;
+  return c;
+}
+
+void oracle_destroy(void* h) { delete (Ctx*)h; }
+
+uint64_t oracle_size(void* h) { return ((Ctx*)h)->table.size(); }
+
+void oracle_params(void* h, uint64_t* B, uint64_t* M) {
+  Ctx* c = (Ctx*)h;
+  *B = c->B;
+  *M = c->M;
+}
+
+uint64_t oracle_sigma(void* h, uint32_t user) { return sigma_of(*(Ctx*)h, user); }
+
+uint64_t oracle_splitmix64(uint64_t x) { return splitmix64(x); }
+uint64_t oracle_fmix64(uint64_t x) { return fmix64(x); }
+
+// Chain values and keys of one prompt of n_blocks full blocks: blocks 1..f are Shared, blocks
+// f+1..n in Iso(user) (f = -1 -> all Shared; f = 0 -> USER_ISOLATION chain from the root).
+void oracle_chain(void* h, const uint32_t* tokens, uint32_t n_blocks, uint32_t user,
+                  int32_t divert_at, uint64_t* S_out, uint64_t* keys_out) {
+  Ctx* c = (Ctx*)h;
+  uint64_t S = 0, Mp = 1;
+  const uint64_t sg = sigma_of(*c, user);
+  for (uint32_t b = 1; b <= n_blocks; ++b) {
+    uint64_t hb = block_hash(*c, tokens + (uint64_t)(b - 1) * c->bs);
+    uint64_t sigma = (divert_at >= 0 && (int64_t)b > (int64_t)divert_at) ? sg : 0;
+    S = chain_step(S, Mp, hb, sigma);
+    Mp = mulmod(Mp, c->M);
+    if (S_out) S_out[b - 1] = S;
+    if (keys_out) keys_out[b - 1] = key_of(S);
+  }
+}
+
+// Validate a whole batch first; no side effects on error.
+//   1: offsets not monotone / offsets[0] != 0   2: token >= 2^20   3: user == NONE
+int oracle_validate(const uint32_t* tokens, const uint64_t* offsets, uint64_t n_req,
+                    const uint32_t* users) {
+  if (offsets[0] != 0) return 1;
+  for (uint64_t j = 0; j < n_req; ++j) {
+    if (offsets[j + 1] < offsets[j]) return 1;
+    if (users[j] == NONE) return 3;
+  }
+  for (uint64_t t = 0; t < offsets[n_req]; ++t)
+    if (tokens[t] >= (1u << 20)) return 2;
+  return 0;
+}
+
+// Admit n_req requests, one at a time, in order.  enforce may be NULL (= all 1,
+// P:726 "detector ... always active").  Returns 0 or a validation error (nothing admitted).
+int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64_t* offsets,
+                   const uint32_t* users, const uint8_t* enforce, oracle_result* out) {
+  Ctx& c = *(Ctx*)h;
+  int err = oracle_validate(tokens, offsets, n_req, users);
+  if (err) return err;
+  std::vector<uint64_t> hsh, S, Kk, I;
+  for (uint64_t j = 0; j < n_req; ++j, ++c.next_seq) {
+    const uint32_t u = users[j];
+    const bool e = enforce ? enforce[j] != 0 : true;
+    const uint32_t* tok = tokens + offsets[j];
+    const uint32_t n = (uint32_t)((offsets[j + 1] - offsets[j]) / c.bs);   // partial tail never
+    // hashed or cached ("block size of 16")
+    hsh.assign(n + 1, 0);
+    for (uint32_t b = 1; b <= n; ++b) hsh[b] = block_hash(c, tok + (uint64_t)(b - 1) * c.bs);
+
+    uint32_t k = 0, r = 0, flagd = 0;
+    int32_t f = -1;
+
+    if (c.policy == 1) {
+      // USER_ISOLATION baseline: a per-user namespace from the root.
+      const uint64_t sg = sigma_of(c, u);
+      I.assign(n + 1, 0);
+      uint64_t T = 0, Mp = 1;
+      for (uint32_t b = 1; b <= n; ++b) {
+        T = chain_step(T, Mp, hsh[b], sg);
+        Mp = mulmod(Mp, c.M);
+        I[b] = key_of(T);
+      }
+      while (r < n && present(c, I[r + 1])) ++r;
+      for (uint32_t b = r + 1; b <= n; ++b) insert_if_absent(c, I[b], u);
+      f = 0;
+    } else {
+      // Shared chain S[b] and keys K[b]
+      S.assign(n + 1, 0);
+      Kk.assign(n + 1, 0);
+      uint64_t Mp = 1;
+      for (uint32_t b = 1; b <= n; ++b) {
+        S[b] = chain_step(S[b - 1], Mp, hsh[b], 0);
+        Mp = mulmod(Mp, c.M);
+        Kk[b] = key_of(S[b]);
+      }
+      // APC lookup: longest present prefix ("partial hits, starting from the beginning of the
+      // prompt"; SPEC lookup_longest_prefix S:99-107).
+      while (k < n && present(c, Kk[k + 1])) ++k;
+
+      if (c.policy == 0) {
+        // Prefix Caching baseline: full reuse, new entries tagged with owner, no flags.
+        r = k;
+        for (uint32_t b = k + 1; b <= n; ++b) insert_if_absent(c, Kk[b], u);
+      } else {
+        // Detector.  Enforcement scan, only while isolation is active:
+        // a hit on a flagged prefix continues only if the NEXT prefix belongs to the requester
+        // (P:458); otherwise reuse stops there (R6, R7).  Flags as of before this request (R10).
+        if (e) {
+          for (uint32_t b = 1; b <= k; ++b) {
+            if (flagged(c, Kk[b]) && !(b < k && owner_of(c, Kk[b + 1]) == u)) {
+              f = (int32_t)b;
+              break;
+            }
+          }
+        }
+        if (f < 0) {
+          // Reuse proceeds.  Hit on an unflagged prefix owned by another user:
+          // "the Detector flags this prefix" — the last reused entry e_r (R2/D2).
+          // Metadata is updated even when isolation is deactivated (R11).
+          r = k;
+          if (k >= 1 && owner_of(c, Kk[k]) != u && !flagged(c, Kk[k])) {
+            c.table.at(Kk[k]).sharer = u;
+            flagd = k;
+          }
+          for (uint32_t b = k + 1; b <= n; ++b) insert_if_absent(c, Kk[b], u);
+        } else {
+          // Selective isolation: reuse stops at the flagged prefix f; the
+          // remaining blocks continue in the requester's isolated namespace rooted at S[f]
+          // (R3): the chain is re-derived step by step with sigma(Iso(u)).
+          const uint64_t sg = sigma_of(c, u);
+          I.assign(n + 1, 0);
+          uint64_t T = S[f];
+          uint64_t Mpf = 1;
+          for (uint32_t b = 1; b <= (uint32_t)f; ++b) Mpf = mulmod(Mpf, c.M);   // M^f
+          for (uint32_t b = (uint32_t)f + 1; b <= n; ++b) {
+            T = chain_step(T, Mpf, hsh[b], sg);
+            Mpf = mulmod(Mpf, c.M);
+            I[b] = key_of(T);
+          }
+          uint32_t m = 0;
+          while ((uint32_t)f + m < n && present(c, I[(uint32_t)f + m + 1])) ++m;
+          r = (uint32_t)f + m;
+          for (uint32_t b = r + 1; b <= n; ++b) insert_if_absent(c, I[b], u);
+        }
+      }
+    }
+    oracle_result& o = out[j];
+    o.n_blocks = n;
+    o.shared_hits = (c.policy == 1) ? 0 : k;
+    o.reused = r;
+    o.divert_at = f;
+    o.flag_depth = flagd;
+    o.bits = (r > 0 ? 1u : 0u) | ((n > 0 && r == n) ? 2u : 0u) | (f >= 0 ? 4u : 0u) |
+             ((f >= 0 && (uint32_t)f < k) ? 8u : 0u) | (flagd > 0 ? 16u : 0u);
+  }
+  return 0;
+}
+
+// Table dump sorted by key.  Returns the number of entries (writes at most cap).
+uint64_t oracle_dump(void* h, oracle_entry* out, uint64_t cap) {
+  Ctx& c = *(Ctx*)h;
+  std::vector<oracle_entry> v;
+  v.reserve(c.table.size());
+  for (auto& kv : c.table) v.push_back(oracle_entry{kv.first, kv.second.owner, kv.second.sharer});
+  std::sort(v.begin(), v.end(),
+            [](const oracle_entry& a, const oracle_entry& b) { return a.key < b.key; });
+  uint64_t n = std::min<uint64_t>(cap, v.size());
+  if (n) std::memcpy(out, v.data(), n * sizeof(oracle_entry));
+  return v.size();
+}
+
+// Copy the table state of one ctx into another (warm-state reuse in tests / bench).
+void oracle_copy_table(void* dst, void* src) { ((Ctx*)dst)->table = ((Ctx*)src)->table; }
+
+void oracle_reserve(void* h, uint64_t n) { ((Ctx*)h)->table.reserve(n); }
+
+}  // extern "C"

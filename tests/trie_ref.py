@@ -1,0 +1,79 @@
+"""Content-keyed trie reference of the DESIGN.md §2 rules (TEST INFRASTRUCTURE, pin I10).
+
+No hashing at all: an entry is named by the block CONTENTS of its path and by its namespace:
+    ("S", (blk_1, ..., blk_b))                        Shared namespace
+    ("I", (blk_1, ..., blk_f), u, (blk_f+1, ..., blk_b))   Iso(u) rooted at the Shared depth f
+USER_ISOLATION uses ("I", (), u, path).  This is a different data structure from the hash-keyed
+dict in oracle/solid_oracle.cpp (keys, namespace salts and the Iso closed form play no role here),
+so agreement pins the oracle's key derivation and namespace handling.  Rules: P:454-459 with the
+DESIGN.md readings R1-R11.
+"""
+from __future__ import annotations
+
+NONE = 0xFFFFFFFF
+
+
+class TrieRef:
+    def __init__(self, block_size: int = 16, policy: int = 2):
+        self.bs = block_size
+        self.policy = policy
+        self.table = {}     # name -> [owner, sharer]
+
+    def _blocks(self, toks):
+        n = len(toks) // self.bs
+        return [tuple(int(t) for t in toks[i * self.bs:(i + 1) * self.bs]) for i in range(n)]
+
+    def admit(self, toks, u: int, e: bool = True):
+        blk = self._blocks(toks)
+        n = len(blk)
+        t = self.table
+        k = r = flagd = 0
+        f = -1
+        if self.policy == 1:
+            names = [("I", (), u, tuple(blk[:b])) for b in range(1, n + 1)]
+            while r < n and names[r] in t:
+                r += 1
+            for b in range(r, n):
+                t.setdefault(names[b], [u, NONE])
+            f = 0
+        else:
+            shared = [("S", tuple(blk[:b])) for b in range(1, n + 1)]
+            while k < n and shared[k] in t:
+                k += 1
+            if self.policy == 0:
+                r = k
+                for b in range(k, n):
+                    t.setdefault(shared[b], [u, NONE])
+            else:
+                if e:
+                    for b in range(1, k + 1):
+                        ent = t[shared[b - 1]]
+                        nxt_own = t[shared[b]][0] if b < k else None
+                        if ent[1] != NONE and not (b < k and nxt_own == u):
+                            f = b
+                            break
+                if f < 0:
+                    r = k
+                    if k >= 1:
+                        ent = t[shared[k - 1]]
+                        if ent[0] != u and ent[1] == NONE:
+                            ent[1] = u
+                            flagd = k
+                    for b in range(k, n):
+                        t.setdefault(shared[b], [u, NONE])
+                else:
+                    root = tuple(blk[:f])
+                    iso = [("I", root, u, tuple(blk[f:b])) for b in range(f + 1, n + 1)]
+                    m = 0
+                    while m < len(iso) and iso[m] in t:
+                        m += 1
+                    r = f + m
+                    for name in iso[m:]:
+                        t.setdefault(name, [u, NONE])
+        bits = ((1 if r > 0 else 0) | (2 if (n > 0 and r == n) else 0) | (4 if f >= 0 else 0)
+                | (8 if (f >= 0 and f < k) else 0) | (16 if flagd > 0 else 0))
+        return (n, 0 if self.policy == 1 else k, r, f, flagd, bits)
+
+    def entries(self):
+        """[(name, owner, sharer)]"""
+        return [(name, v[0], v[1]) for name, v in self.table.items()]
