@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Benchmark: prefix lookups/s of the CacheSolidarity hot path on B200 (BASELINE.json metric).
+
+A step = one batch admission (solid_lookup_batch + solid_insert_batch: hash, scan, probe, Detector
+resolution, commit) of the C2 workload (BASELINE configs[1]: 1000 users x 100 requests x 2000
+tokens, 80% common system prompt), inputs resident in HBM, on an index restored to the same
+(empty) pre-batch state before every step (restore is outside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+N > 1 (torchrun, one process per GPU): every rank admits its own independent tenant partition
+(weak scaling, no data-path collective; the hash-sharded single index is DESIGN.md §7 NEXT); the
+time is the max over ranks.  `--impl reference` times the sequential CPU oracle on the same
+workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefix lookups/sec (requests & blocks) at 1/2/4/8 B200; % HBM roofline"
+SEED = 0x5011D000
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _workload(name: str, rank: int):
+    from workloads import c2_shared_prompt
+    if name == "c2":
+        s = c2_shared_prompt(seed=SEED + 2 + 1000 * rank)
+        desc = ("c2_shared_prompt: 1000 users x 100 requests, 2000-token prompts (1600-token common "
+                "system prompt = 80%, 256-token per-user profile, 144 fresh), one 100k-request batch")
+        return s, desc
+    if name == "c2_small":
+        s = c2_shared_prompt(users=100, reqs_per_user=100, seed=SEED + 2 + 1000 * rank)
+        return s, "c2_shared_prompt scaled to 100 users x 100 requests (quick check)"
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.path = gpu, None, None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    sm.append(float(parts[0])); mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[2:]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(stream, sample_requests: int):
+    """The oracle as it stands (sequential, one thread) on the first `sample_requests` requests."""
+    from oracle import Oracle
+    s = stream.slice(0, min(sample_requests, stream.n_requests))
+    o = Oracle(16, SEED, 2)
+    o.reserve(s.n_blocks() // 8 + 1024)
+    t0 = time.perf_counter()
+    o.process(s)
+    dt = time.perf_counter() - t0
+    return {"value": s.n_requests / dt, "unit": "requests/s", "cores": 1, "kind": "oracle",
+            "blocks_per_s": s.n_blocks() / dt, "seconds": dt,
+            "sample": f"first {s.n_requests} requests ({s.n_blocks()} blocks) of the same stream, "
+                      f"sequential C++ oracle, 1 thread (host has {os.cpu_count()} cores)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    stream, desc = _workload(args.config, 0)
+    from oracle import Oracle
+    n_sample = min(stream.n_requests, args.ref_sample)
+    s = stream.slice(0, n_sample)
+    times = []
+    for step in range(args.warmup + args.steps):
+        o = Oracle(16, SEED, 2)
+        o.reserve(s.n_blocks() // 8 + 1024)
+        t0 = time.perf_counter()
+        o.process(s)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    v = n_sample * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "requests/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "blocks_per_s": s.n_blocks() * args.steps / tot,
+            "config": {"workload": desc, "policy": "solidarity",
+                       "sample": f"first {n_sample} requests per step"},
+            "cpu_baseline": {"value": v, "unit": "requests/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first {n_sample} requests ({s.n_blocks()} blocks) of the "
+                                       f"workload per step, sequential oracle, 1 thread"},
+            "e2e": {"value": v, "unit": "requests/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=100_000)
+    ap.add_argument("--ref-sample", type=int, default=20_000)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2603_10726_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    stream_np, desc = _workload(args.config, rank)
+    N = stream_np.n_requests
+    nblk = stream_np.n_blocks()
+    dev = torch.device("cuda", local)
+    d = P.to_device(stream_np, dev)
+    idx = P.Index("solidarity", capacity_blocks=max(2 * nblk // 10, 1 << 20),
+                  max_batch_tokens=stream_np.n_tokens + 64, max_batch_requests=N,
+                  seed=SEED, device=local)
+    out = torch.empty((N, 6), dtype=torch.int32, device=dev)
+    cs = torch.cuda.current_stream(dev)
+
+    def step():
+        idx.lookup(d["tokens"], d["offsets"], d["users"], d["enforce"], out=out)
+        idx.insert()
+
+    # warm-up
+    for _ in range(args.warmup):
+        idx.reset()
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    phase = {"hash": [], "resolve": [], "commit": [], "hash_kernel": [], "round1": []}
+    rounds, launches = [], []
+    stats = None
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            idx.reset()                 # restore the empty pre-batch index (outside events)
+            ev[k][0].record(cs)
+            step()
+            ev[k][1].record(cs)
+            stats = idx.stats()
+            for key, f in [("hash", "ms_hash"), ("resolve", "ms_resolve"),
+                           ("commit", "ms_commit"), ("hash_kernel", "ms_hash_kernel"),
+                           ("round1", "ms_round_first")]:
+                phase[key].append(stats[f])
+            rounds.append(stats["last_rounds"])
+            launches.append(stats["last_kernel_launches"])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    clocks = clk.summary()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(ms)
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    reqs_all = N * world
+    value = reqs_all * args.steps / (tot_ms / 1000.0)
+
+    # correctness spot-check of the timed configuration (full check lives in tests/)
+    res = P.as_numpy(out)
+
+    # roofline of the dominant kernel
+    peak, peak_src = _peaks()
+    alg_bytes = stats["algorithmic_bytes"]
+    hash_ms = statistics.median(phase["hash_kernel"])
+    hash_bytes = 64 * nblk + 12 * N + 4 * nblk
+    step_ms = tot_ms / args.steps
+    roof_step = alg_bytes / (step_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_hash_register (hash + scan + probe/register)",
+                "achieved": hash_bytes / (hash_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": hash_bytes / (hash_ms / 1e3) / 1e9 / peak, "traffic": None,
+                "algorithmic_bytes_per_launch": hash_bytes, "launch_ms": hash_ms,
+                "peak_source": peak_src,
+                "whole_step": {"achieved": roof_step, "frac": roof_step / peak,
+                               "algorithmic_bytes": alg_bytes}}
+
+    # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.profile and args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+        ht, ho, hu = pin(stream_np.tokens), pin(stream_np.offsets), pin(stream_np.users)
+        hout = np.zeros(N, dtype=P.RESULT_DTYPE)
+        idx.reset()
+        idx.admit_host(ht, ho, hu, None, out=hout)
+        e2e_t = 0.0
+        for _ in range(args.e2e_steps):
+            idx.reset()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            idx.admit_host(ht, ho, hu, None, out=hout)
+            e2e_t += time.perf_counter() - t0
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": reqs_all * args.e2e_steps / float(tt.item()), "unit": "requests/s",
+               "h2d_bytes_per_step": int(ht.nbytes + ho.nbytes + hu.nbytes),
+               "d2h_bytes_per_step": int(hout.nbytes),
+               "how": "solid_admit_host: pinned host buffers -> H2D -> lookup -> insert -> D2H, "
+                      "host wall clock (perf_counter) around the call"}
+        assert (hout["reused"] == res["reused"]).all()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
+        cpu = cpu_baseline(stream_np, args.cpu_sample)
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "blocks_per_s": nblk * world * args.steps / (tot_ms / 1000.0),
+            "config": {"workload": desc, "policy": "solidarity", "batch_requests": N,
+                       "blocks_per_batch": nblk, "tokens_per_batch": stream_np.n_tokens,
+                       "parallelism": f"{world} independent tenant partitions (weak)",
+                       "l2": "inputs (800 MB tokens) larger than L2 (126 MB); no flush",
+                       "restore": "index reset to empty before every step, outside the events"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(sum(launches)),
+            "clocks": clocks,
+            "phases_ms_median": {k: statistics.median(v) for k, v in phase.items() if v},
+            "resolver_rounds": rounds[-1] if rounds else None,
+            "step_ms": ms,
+            "result_summary": {"reused_blocks": int(res["reused"].sum()),
+                               "diverted": int(((res["bits"] & 4) > 0).sum()),
+                               "flagged": int(((res["bits"] & 16) > 0).sum()),
+                               "entries": int(stats["live_entries"])},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/*
+ * solid.h — C ABI of the B200-native CacheSolidarity hot path.
+ *
+ * One context = one GPU-resident prefix index (open addressing, 16-byte slots {key, owner,
+ * sharer}) plus per-batch scratch.  A batch of requests is admitted with solid_lookup_batch
+ * (hash -> chained keys -> longest cached prefix -> Detector decision)
+ * followed by solid_insert_batch (new entries tagged with the requester, and
+ * AttackFlag/sharer writes).  The pair equals admitting the batch's requests one at a time
+ * in sequence order (R1): results never depend on how a stream is cut into batches.
+ *
+ * Conventions
+ *   - All functions return solid_status.  Invalid arguments -> SOLID_ERR_INVALID with no side
+ *     effect on the index.  Capacity overflow -> SOLID_ERR_CAPACITY with no mutation (R9).
+ *     A CUDA failure -> SOLID_ERR_CUDA and the context is poisoned (later calls return
+ *     SOLID_ERR_STATE).  solid_last_error() returns a message for the last failure.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is
+ *     enqueued on it; solid_lookup_batch blocks the calling thread once per batch to read the
+ *     resolver's convergence flags (host-polled resolver).
+ *   - Device pointers are caller-owned and must stay valid until the call returns (lookup reads
+ *     them until the resolver converged; it synchronises `stream` before returning).
+ *   - A context is single-writer (SPEC S:148 single stream); distinct contexts are independent.
+ */
+#ifndef SOLID_H
+#define SOLID_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SOLID_ABI_VERSION 1u
+#define SOLID_USER_NONE 0xFFFFFFFFu   /* "no user": sharer of an unflagged entry */
+
+typedef enum {
+  SOLID_OK = 0,
+  SOLID_ERR_INVALID = 1,   /* bad argument / batch (token >= 2^20, user == NONE, offsets ...)  */
+  SOLID_ERR_CAPACITY = 2,  /* index or scratch would overflow; nothing was mutated             */
+  SOLID_ERR_STATE = 3,     /* call order violated, or context poisoned by an earlier failure  */
+  SOLID_ERR_CUDA = 4,      /* CUDA runtime error (context poisoned)                           */
+  SOLID_ERR_NCCL = 5,      /* reserved for the sharded multi-GPU index          */
+  SOLID_ERR_OOM = 6        /* device allocation failed in solid_init                          */
+} solid_status;
+
+typedef enum {
+  SOLID_POLICY_APC = 0,            /* Prefix Caching baseline: full reuse, no flags    */
+  SOLID_POLICY_USER_ISOLATION = 1, /* User Cache Isolation baseline (reading R4)   */
+  SOLID_POLICY_SOLIDARITY = 2      /* CacheSolidarity: Detector + selective isolation */
+} solid_policy;
+
+typedef struct {
+  uint32_t block_size;         /* tokens per cache entry; must be 16 (reading R13)       */
+  uint32_t max_blocks;         /* max full blocks per request (power tables); e.g. 8192          */
+  uint64_t capacity_blocks;    /* max live entries in the index (no eviction, R9)               */
+  uint64_t max_batch_tokens;   /* scratch sizing: max tokens per batch                           */
+  uint64_t max_batch_requests; /* scratch sizing: max requests per batch                         */
+  uint64_t hash_seed;          /* H-def v2 seed; secret per deployment          */
+  int32_t policy;              /* solid_policy                                                   */
+  int32_t device;              /* CUDA device ordinal                                            */
+} solid_config;
+
+typedef struct solid_ctx solid_ctx;
+
+/* One batch in global sequence order (CSR).  Pointers are DEVICE memory for
+ * solid_lookup_batch and HOST memory for solid_admit_host. */
+typedef struct {
+  uint64_t n_requests;
+  const uint32_t* tokens;   /* concatenated token ids, each < 2^20 (R15); 4-byte aligned.
+                               Loads may touch up to 12 bytes past a request's last full block
+                               within the same 16-byte granule.                                  */
+  const uint64_t* offsets;  /* n_requests+1, offsets[0] == 0, non-decreasing; request j =
+                               tokens[offsets[j], offsets[j+1]); its floor(len/16) full blocks are
+                               hashed, the tail is never cached                  */
+  const uint32_t* users;    /* requester ids, != SOLID_USER_NONE                                */
+  const uint8_t* enforce;   /* per-request isolation-active bit (Activator output); NULL
+                               = all 1.  enforce=0 still updates metadata (R11)   */
+} solid_batch;
+
+/* Per-request result, 24 bytes. */
+typedef struct {
+  uint32_t n_blocks;     /* floor(len / 16)                                                    */
+  uint32_t shared_hits;  /* k: Shared hit-chain length (USER_ISOLATION: 0)                    */
+  uint32_t reused;       /* r: blocks whose cached content is served                          */
+  int32_t divert_at;     /* f: depth where reuse left the Shared chain, -1 none (USER_ISO: 0) */
+  uint32_t flag_depth;   /* depth of the entry this request flagged, 0 = none                 */
+  uint32_t bits;         /* HIT=1 (r>0) FULL=2 (n>0,r==n) DIVERTED=4 TRUNCATED=8 (f<k) FLAGGED=16 */
+} solid_result;
+
+enum { SOLID_HIT = 1, SOLID_FULL = 2, SOLID_DIVERTED = 4, SOLID_TRUNCATED = 8, SOLID_FLAGGED = 16 };
+
+typedef struct {
+  uint64_t key;      /* block key (H-def v2)                                                  */
+  uint32_t owner;    /* OwnerID: set once at allocation                              */
+  uint32_t sharer;   /* user that flagged it; AttackFlag <=> sharer != SOLID_USER_NONE (R5)  */
+} solid_entry;
+
+typedef struct {
+  /* cumulative over all committed batches */
+  uint64_t batches, requests, blocks, reused_blocks, inserted, flagged, diverted, truncated;
+  uint64_t live_entries;
+  /* last batch */
+  uint32_t last_rounds;          /* resolver rounds until the sequential fixed point         */
+  uint32_t last_distinct_keys;   /* scratch keys registered (Shared + isolated) last batch   */
+  uint64_t last_requests, last_blocks, last_inserted, last_flagged;
+  float ms_hash, ms_resolve, ms_commit;    /* device time per phase of the last batch       */
+  uint64_t algorithmic_bytes;    /* DESIGN.md §5 formula for the last batch                  */
+  uint64_t last_kernel_launches; /* kernels this library launched for the last batch         */
+  float ms_hash_kernel;          /* device time of k_hash_register alone (last batch)        */
+  float ms_round_first;          /* device time of the first resolver round (last batch)     */
+} solid_stats_t;
+
+uint32_t solid_abi_version(void);
+
+/* Allocate the index (2^ceil(log2(2*capacity)) slots) and scratch on cfg->device. */
+solid_status solid_init(const solid_config* cfg, solid_ctx** out);
+solid_status solid_destroy(solid_ctx* ctx);
+
+/* Lookup + Detector for one batch (device pointers).  Writes out[n_requests] (DEVICE memory)
+ * and stages every mutation (new entries, new flags); the persistent index is only read.
+ * Request i of the batch has global sequence position (earlier batches) + i.
+ * Must be followed by solid_insert_batch before the next lookup (else SOLID_ERR_STATE). */
+solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* batch, solid_result* out,
+                                void* stream);
+
+/* Commit the staged admissions of the last lookup: 128-bit CAS claims {key, owner, sharer}
+ * for new entries and sharer writes on flagged existing entries.  Checks capacity first. */
+solid_status solid_insert_batch(solid_ctx* ctx, void* stream);
+
+/* lookup + insert with HOST buffers: copies the batch to the device, admits it, copies the
+ * results back to out_host (HOST memory) and synchronises `stream`. */
+solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* host_batch,
+                              solid_result* out_host, void* stream);
+
+solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out);
+
+/* Copy live entries to host_out (HOST memory, capacity `cap` entries) sorted by key; *n_out =
+ * number of live entries (may exceed cap; then only cap are written). */
+solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64_t cap, uint64_t* n_out);
+
+/* Empty the index and all scratch (keeps allocations). */
+solid_status solid_reset(solid_ctx* ctx);
+
+/* Save / restore the index contents into / from a ctx-owned device buffer (warm-state reuse). */
+solid_status solid_checkpoint(solid_ctx* ctx);
+solid_status solid_restore(solid_ctx* ctx);
+
+const char* solid_last_error(const solid_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOLID_H */

@@ -1,0 +1,241 @@
+"""Python binding of the B200-native CacheSolidarity hot path (include/solid.h).
+
+Argument marshalling only: every step of the path runs in the CUDA kernels of lib/libsolid.so.
+PyTorch provides device memory and streams.  There is NO CPU fallback — importing this package
+on a machine without the built library raises, and Index() needs a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libsolid.so")
+
+SOLID_OK, SOLID_ERR_INVALID, SOLID_ERR_CAPACITY, SOLID_ERR_STATE, SOLID_ERR_CUDA, \
+    SOLID_ERR_NCCL, SOLID_ERR_OOM = range(7)
+POLICY = {"apc": 0, "user_isolation": 1, "solidarity": 2}
+HIT, FULL, DIVERTED, TRUNCATED, FLAGGED = 1, 2, 4, 8, 16
+USER_NONE = 0xFFFFFFFF
+
+RESULT_DTYPE = np.dtype([("n_blocks", "<u4"), ("shared_hits", "<u4"), ("reused", "<u4"),
+                         ("divert_at", "<i4"), ("flag_depth", "<u4"), ("bits", "<u4")])
+ENTRY_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4")])
+
+# C ABI entry points declared in include/solid.h (checked by tests/test_abi.py)
+ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
+               "solid_insert_batch", "solid_admit_host", "solid_stats", "solid_dump",
+               "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error"]
+
+
+class SolidError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"solid status {status}: {msg}")
+        self.status = status
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("block_size", ctypes.c_uint32), ("max_blocks", ctypes.c_uint32),
+                ("capacity_blocks", ctypes.c_uint64), ("max_batch_tokens", ctypes.c_uint64),
+                ("max_batch_requests", ctypes.c_uint64), ("hash_seed", ctypes.c_uint64),
+                ("policy", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+class _Batch(ctypes.Structure):
+    _fields_ = [("n_requests", ctypes.c_uint64), ("tokens", ctypes.c_void_p),
+                ("offsets", ctypes.c_void_p), ("users", ctypes.c_void_p),
+                ("enforce", ctypes.c_void_p)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("batches", ctypes.c_uint64), ("requests", ctypes.c_uint64),
+                ("blocks", ctypes.c_uint64), ("reused_blocks", ctypes.c_uint64),
+                ("inserted", ctypes.c_uint64), ("flagged", ctypes.c_uint64),
+                ("diverted", ctypes.c_uint64), ("truncated", ctypes.c_uint64),
+                ("live_entries", ctypes.c_uint64), ("last_rounds", ctypes.c_uint32),
+                ("last_distinct_keys", ctypes.c_uint32), ("last_requests", ctypes.c_uint64),
+                ("last_blocks", ctypes.c_uint64), ("last_inserted", ctypes.c_uint64),
+                ("last_flagged", ctypes.c_uint64), ("ms_hash", ctypes.c_float),
+                ("ms_resolve", ctypes.c_float), ("ms_commit", ctypes.c_float),
+                ("algorithmic_bytes", ctypes.c_uint64),
+                ("last_kernel_launches", ctypes.c_uint64), ("ms_hash_kernel", ctypes.c_float),
+                ("ms_round_first", ctypes.c_float)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsolid.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -m paper_2603_10726_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, st = ctypes.c_void_p, ctypes.c_int
+    lib.solid_abi_version.restype = ctypes.c_uint32
+    lib.solid_init.restype = st
+    lib.solid_init.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(vp)]
+    lib.solid_destroy.restype = st
+    lib.solid_destroy.argtypes = [vp]
+    lib.solid_lookup_batch.restype = st
+    lib.solid_lookup_batch.argtypes = [vp, ctypes.POINTER(_Batch), vp, vp]
+    lib.solid_insert_batch.restype = st
+    lib.solid_insert_batch.argtypes = [vp, vp]
+    lib.solid_admit_host.restype = st
+    lib.solid_admit_host.argtypes = [vp, ctypes.POINTER(_Batch), vp, vp]
+    lib.solid_stats.restype = st
+    lib.solid_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
+    lib.solid_dump.restype = st
+    lib.solid_dump.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+    for name in ["solid_reset", "solid_checkpoint", "solid_restore"]:
+        getattr(lib, name).restype = st
+        getattr(lib, name).argtypes = [vp]
+    lib.solid_last_error.restype = ctypes.c_char_p
+    lib.solid_last_error.argtypes = [vp]
+    _lib = lib
+    return lib
+
+
+def _np_ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+class Index:
+    """One GPU-resident prefix index (C ABI context).
+
+    lookup(...) + insert() admit one batch; results are a torch int32 tensor [N, 6] on the device
+    (fields of RESULT_DTYPE).  `as_numpy(results)` converts a host copy to the structured dtype.
+    """
+
+    def __init__(self, policy: str = "solidarity", capacity_blocks: int = 1 << 20,
+                 max_batch_tokens: int = 1 << 24, max_batch_requests: int = 1 << 16,
+                 max_blocks: int = 8192, seed: int = 0x5011D000, device: int = 0):
+        self.lib = load_library()
+        cfg = _Config(16, max_blocks, capacity_blocks, max_batch_tokens, max_batch_requests,
+                      seed & 0xFFFFFFFFFFFFFFFF, POLICY[policy], device)
+        h = ctypes.c_void_p()
+        rc = self.lib.solid_init(ctypes.byref(cfg), ctypes.byref(h))
+        if rc != SOLID_OK:
+            raise SolidError(rc, "solid_init failed (needs a CUDA device and valid sizes)")
+        self.h = h
+        self.device = device
+        self.policy = policy
+        self.seed = seed
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.solid_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc != SOLID_OK:
+            msg = self.lib.solid_last_error(self.h)
+            raise SolidError(rc, msg.decode() if msg else "")
+
+    @staticmethod
+    def _stream(stream):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        return ctypes.c_void_p(stream.cuda_stream)
+
+    # ---- device-buffer admission ---------------------------------------------------------
+    def lookup(self, tokens, offsets, users, enforce=None, out=None, stream=None):
+        """tokens int32/uint32 [T], offsets int64 [N+1], users int32/uint32 [N], enforce uint8
+        [N] or None — all CUDA tensors.  Returns the result tensor (int32 [N, 6])."""
+        import torch
+        n = int(users.numel())
+        if out is None:
+            out = torch.empty((max(n, 1), 6), dtype=torch.int32, device=offsets.device)
+        for t in (tokens, offsets, users, out) + ((enforce,) if enforce is not None else ()):
+            if not t.is_cuda or not t.is_contiguous():
+                raise ValueError("batch tensors must be contiguous CUDA tensors")
+        b = _Batch(n, tokens.data_ptr(), offsets.data_ptr(), users.data_ptr(),
+                   enforce.data_ptr() if enforce is not None else None)
+        self._check(self.lib.solid_lookup_batch(self.h, ctypes.byref(b),
+                                                ctypes.c_void_p(out.data_ptr()),
+                                                self._stream(stream)))
+        return out[:n]
+
+    def insert(self, stream=None):
+        self._check(self.lib.solid_insert_batch(self.h, self._stream(stream)))
+
+    def admit(self, tokens, offsets, users, enforce=None, out=None, stream=None):
+        out = self.lookup(tokens, offsets, users, enforce, out, stream)
+        self.insert(stream)
+        return out
+
+    # ---- host-buffer admission (copies inside the C ABI call) -----------------------------
+    def admit_host(self, tokens: np.ndarray, offsets: np.ndarray, users: np.ndarray,
+                   enforce: Optional[np.ndarray] = None, out: Optional[np.ndarray] = None,
+                   stream=None) -> np.ndarray:
+        tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        users = np.ascontiguousarray(users, dtype=np.uint32)
+        en = None if enforce is None else np.ascontiguousarray(enforce, dtype=np.uint8)
+        n = users.shape[0]
+        if out is None:
+            out = np.zeros(max(n, 1), dtype=RESULT_DTYPE)
+        if tokens.size == 0:
+            tokens = np.zeros(4, np.uint32)
+        b = _Batch(n, _np_ptr(tokens), _np_ptr(offsets), _np_ptr(users), _np_ptr(en))
+        self._check(self.lib.solid_admit_host(self.h, ctypes.byref(b),
+                                              ctypes.c_void_p(out.ctypes.data),
+                                              self._stream(stream)))
+        return out[:n]
+
+    # ---- inspection / state --------------------------------------------------------------
+    def stats(self) -> dict:
+        s = _Stats()
+        self._check(self.lib.solid_stats(self.h, ctypes.byref(s)))
+        return {name: getattr(s, name) for name, _ in _Stats._fields_}
+
+    def dump(self) -> np.ndarray:
+        n = ctypes.c_uint64()
+        self._check(self.lib.solid_dump(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros(max(int(n.value), 1), dtype=ENTRY_DTYPE)
+        self._check(self.lib.solid_dump(self.h, ctypes.c_void_p(out.ctypes.data), n.value,
+                                        ctypes.byref(n)))
+        return out[:int(n.value)]
+
+    def reset(self):
+        self._check(self.lib.solid_reset(self.h))
+
+    def checkpoint(self):
+        self._check(self.lib.solid_checkpoint(self.h))
+
+    def restore(self):
+        self._check(self.lib.solid_restore(self.h))
+
+
+def as_numpy(results) -> np.ndarray:
+    """int32 [N, 6] result tensor/array -> structured RESULT_DTYPE array (host)."""
+    if hasattr(results, "cpu"):
+        results = results.cpu().numpy()
+    return np.ascontiguousarray(results).view(RESULT_DTYPE).reshape(-1)
+
+
+def to_device(stream_obj, device="cuda"):
+    """workloads.Stream -> dict of CUDA tensors for Index.lookup (marshalling helper)."""
+    import torch
+    tok = torch.from_numpy(stream_obj.tokens.view(np.int32)).to(device)
+    if tok.numel() == 0:
+        tok = torch.zeros(4, dtype=torch.int32, device=device)
+    d = dict(tokens=tok,
+             offsets=torch.from_numpy(stream_obj.offsets.view(np.int64)).to(device),
+             users=torch.from_numpy(stream_obj.users.view(np.int32)).to(device),
+             enforce=None if stream_obj.enforce is None else
+             torch.from_numpy(stream_obj.enforce).to(device))
+    return d

@@ -1,0 +1,1134 @@
+// solid.cu — B200 (sm_100a) kernels + host runtime behind include/solid.h.
+//
+// Hot path of one batch:
+//   K_A  k_hash_register   tokens -> per-block hash (a2) -> chained-prefix scan (a3) -> key ->
+//                          register in the batch scratch table (a4; probes the index once per
+//                          distinct key) -> APC first-occurrence guess
+//   K_B  k_eval<POLICY>    per-request first miss (a5, warp ballot), barrier scan, isolated walk,
+//                          flag decision, seq-min scatter of staged inserts/flags  — repeated
+//                          (Jacobi rounds) until no decision changes = the sequential answer (R1)
+//   K_C  k_commit          128-bit CAS claims {key, owner, sharer} + sharer writes (a6)
+//   K_D  k_stats / k_cleanup
+//
+// Sequence tags.  Every staged value is a u64 (tag << 32 | seq') with tag = ~(epoch*4096 + sub),
+// seq' = batch position + 1, sub = 0 (round-0 guess), t (round t), 4095 (index snapshot).  atomicMin
+// keeps the EARLIEST request of the newest tag, so stale rounds/batches never need clearing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "solid.h"
+#include "solid_math.cuh"
+
+namespace solid {
+
+constexpr int kNSeg = 128;            // created-list segments (spread the append atomics)
+constexpr uint32_t kSubSnap = 4095;
+constexpr uint32_t kMaxRounds = 4093;
+constexpr uint32_t kMaxEpoch = (0xFFFFFFFFu / 4096u) - 1;
+
+enum : uint32_t {
+  ERR_OFFSETS = 1, ERR_TOKEN = 2, ERR_USER = 4, ERR_BLOCKS = 8, ERR_SCRATCH = 16, ERR_SLOTCAP = 32
+};
+
+// 64-byte scratch slot: one key of the batch (Shared or isolated) and its staged state.
+struct __align__(64) Slot {
+  unsigned long long key;          // 0 = empty
+  uint32_t snap_owner;             // owner in the index at batch start, kNone = absent
+  uint32_t snap_sharer;            // sharer in the index at batch start
+  uint32_t psl;                    // index slot of the snapshot entry
+  uint32_t pad[3];
+  unsigned long long st[4];        // ping-pong: [0]=P0.ins [1]=P0.flg [2]=P1.ins [3]=P1.flg
+};
+static_assert(sizeof(Slot) == 64, "slot layout");
+
+struct DevStatus {
+  uint32_t err;
+  uint32_t pad;
+  unsigned long long new_entries;        // k_commit count mode
+  unsigned long long new_flags;          // flags on index (snapshot) entries
+  unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
+  uint32_t changed[kMaxRounds + 2];
+};
+
+struct KParams {
+  uint32_t klo[kBS], khi[kBS];     // K_i = B^i split in 32-bit limbs
+  const unsigned long long* mpow;  // M^i, i < max_blocks
+  const unsigned long long* gtab;  // G[d] = sum_{t<d} M^t, d <= max_blocks
+  uint64_t seed;
+  const uint32_t* tokens;
+  const uint64_t* offsets;
+  const uint32_t* users;
+  const uint8_t* enforce;
+  uint64_t n;
+  uint32_t max_blocks;
+  uint32_t epoch;
+  Slot* sl;
+  uint64_t smask;
+  ulonglong2* tab;
+  uint64_t tmask;
+  uint32_t* slot_of_block;
+  uint64_t slot_cap;
+  uint4* dec;
+  solid_result* out;
+  uint32_t* seg_cnt;
+  uint32_t* seg_list;
+  uint32_t seg_cap;
+  DevStatus* st;
+};
+
+__host__ __device__ __forceinline__ uint32_t tag_of(uint32_t epoch, uint32_t sub) {
+  return 0xFFFFFFFFu - (epoch * 4096u + sub);
+}
+
+__device__ __forceinline__ void set_err(DevStatus* st, uint32_t bits) { atomicOr(&st->err, bits); }
+
+__device__ __forceinline__ uint4 ldg_v4(const uint32_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ ulonglong2 ld_v2u64(const void* p) {
+  ulonglong2 r;
+  asm volatile("ld.global.v2.u64 {%0,%1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+  return r;
+}
+
+// 128-bit compare-and-swap (ATOMG.E.CAS.128 on sm_90+).
+__device__ __forceinline__ ulonglong2 atomic_cas128(ulonglong2* addr, ulonglong2 cmp,
+                                                    ulonglong2 val) {
+  ulonglong2 old;
+  asm volatile(
+      "{\n\t.reg .b128 c, v, d;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(old.x), "=l"(old.y)
+      : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(addr)
+      : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void atomic_min_u64(unsigned long long* a, unsigned long long v) {
+  // read-before-atomic: values only ever decrease, so a stale read is >= the true value.
+  if (*(volatile unsigned long long*)a > v) atomicMin(a, v);
+}
+
+// ---------------------------------------------------------------------------------------------
+// a2: per-block hash h = sum_i (tok_i + 1) * K_i mod p over one 16-token block.
+// `sh` = (address / 4) mod 4 is warp-uniform (all blocks of a request share it).
+// ---------------------------------------------------------------------------------------------
+template <int SH>
+__device__ __forceinline__ uint64_t hash16(const uint32_t* p, const KParams& kp, uint32_t& bad) {
+  uint32_t t[16];
+  if (SH == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 v = ldg_v4(p + 4 * q);
+      t[4 * q] = v.x; t[4 * q + 1] = v.y; t[4 * q + 2] = v.z; t[4 * q + 3] = v.w;
+    }
+  } else {
+    uint32_t w[20];
+    const uint32_t* a = p - SH;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      uint4 v = ldg_v4(a + 4 * q);
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = w[i + SH];
+  }
+  uint64_t lo = 0, hi = 0;
+  uint32_t orv = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    orv |= t[i];
+    const uint32_t x = t[i] + 1u;
+    lo += (uint64_t)x * kp.klo[i];
+    hi += (uint64_t)x * kp.khi[i];
+  }
+  bad |= orv >> 20;
+  // lo + hi*2^32 mod p, with hi*2^32 = (hi mod 2^29)*2^32 + (hi >> 29)*2^61 == ... + (hi >> 29)
+  return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
+}
+
+__device__ __forceinline__ uint64_t hash_block(const uint32_t* p, int sh, const KParams& kp,
+                                               uint32_t& bad) {
+  switch (sh) {
+    case 0: return hash16<0>(p, kp, bad);
+    case 1: return hash16<1>(p, kp, bad);
+    case 2: return hash16<2>(p, kp, bad);
+    default: return hash16<3>(p, kp, bad);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Index (persistent table) probe: linear probing over 16-byte slots {key, owner | sharer << 32}.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool index_find(const KParams& kp, uint64_t key, uint32_t& owner,
+                                           uint32_t& sharer, uint64_t& pos) {
+  pos = key & kp.tmask;
+  for (;;) {
+    ulonglong2 e = ld_v2u64(&kp.tab[pos]);
+    if (e.x == key) {
+      owner = (uint32_t)e.y;
+      sharer = (uint32_t)(e.y >> 32);
+      return true;
+    }
+    if (e.x == 0) return false;
+    pos = (pos + 1) & kp.tmask;
+  }
+}
+
+__device__ __forceinline__ uint64_t scratch_home(uint64_t key, uint64_t mask) {
+  return (key ^ (key >> 29)) & mask;
+}
+
+// First touch of a scratch slot in this batch: record the index snapshot of the key and seed
+// both ping-pong states with it (snapshot tag = the smallest tag of the batch).
+__device__ void init_slot(const KParams& kp, Slot* s, uint64_t key) {
+  uint32_t owner = kNone, sharer = kNone;
+  uint64_t ipos = 0;
+  const bool present = index_find(kp, key, owner, sharer, ipos);
+  s->snap_owner = present ? owner : kNone;
+  s->snap_sharer = present ? sharer : kNone;
+  s->psl = present ? (uint32_t)ipos : kNone;
+  if (present) {
+    const unsigned long long v = (unsigned long long)tag_of(kp.epoch, kSubSnap) << 32;
+    atomicMin(&s->st[0], v);
+    atomicMin(&s->st[2], v);
+    if (sharer != kNone) {
+      atomicMin(&s->st[1], v);
+      atomicMin(&s->st[3], v);
+    }
+  }
+}
+
+// Find-or-insert `key` in the scratch table.  Returns the slot index; `created` is set for the
+// thread that claimed it.  Keys are never removed during a batch (k_cleanup clears them after).
+__device__ __forceinline__ uint64_t scratch_register(const KParams& kp, uint64_t key,
+                                                     bool& created) {
+  uint64_t pos = scratch_home(key, kp.smask);
+  for (uint64_t probes = 0;; ++probes) {
+    Slot* s = kp.sl + pos;
+    unsigned long long k = *(volatile unsigned long long*)&s->key;
+    if (k == key) return pos;
+    if (k == 0) {
+      unsigned long long old = atomicCAS(&s->key, 0ull, (unsigned long long)key);
+      if (old == 0) {
+        created = true;
+        init_slot(kp, s, key);
+        return pos;
+      }
+      if (old == key) return pos;
+    }
+    pos = (pos + 1) & kp.smask;
+    if (probes > kp.smask) {
+      set_err(kp.st, ERR_SCRATCH);
+      return ~0ull;
+    }
+  }
+}
+
+__device__ __forceinline__ bool scratch_find(const KParams& kp, uint64_t key, uint64_t& pos) {
+  pos = scratch_home(key, kp.smask);
+  for (uint64_t probes = 0; probes <= kp.smask; ++probes) {
+    unsigned long long k = *(volatile unsigned long long*)&kp.sl[pos].key;
+    if (k == key) return true;
+    if (k == 0) return false;
+    pos = (pos + 1) & kp.smask;
+  }
+  return false;
+}
+
+// Warp-aggregated append of newly created slots to the created list (for k_cleanup).
+__device__ __forceinline__ void append_created(const KParams& kp, bool created, uint64_t pos,
+                                               int lane, uint32_t seg) {
+  const uint32_t m = __ballot_sync(0xffffffffu, created);
+  if (!m) return;
+  uint32_t base = 0;
+  if (lane == 0) base = atomicAdd(&kp.seg_cnt[seg], (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (created) {
+    const uint32_t idx = base + __popc(m & ((1u << lane) - 1u));
+    if (idx < kp.seg_cap) kp.seg_list[(uint64_t)seg * kp.seg_cap + idx] = (uint32_t)pos;
+    else set_err(kp.st, ERR_SCRATCH);
+  }
+}
+
+// Is a staged value (tag << 32 | seq') visible to request seq' = seqp, reading round tag `tagR`?
+__device__ __forceinline__ bool staged_visible(unsigned long long v, uint32_t seqp, uint32_t tagR,
+                                               uint32_t tagS) {
+  const uint32_t tg = (uint32_t)(v >> 32);
+  return tg == tagS || (tg == tagR && (uint32_t)v < seqp);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K_A (round 0): hash + chained-prefix scan + registration.  One warp per request; lane = block
+// within a 32-block group.  Forward-exponent chain:
+//   S[b] = sum_{t<=b} M^(t-1) * (h_t + sigma)   — a prefix SUM: warp shfl scan + scalar carry.
+// ---------------------------------------------------------------------------------------------
+template <int POLICY>
+__global__ void __launch_bounds__(256) k_hash_register(KParams kp) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= kp.n) return;
+  const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
+  const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
+  const uint32_t u = kp.users[j];
+  if (lane == 0) {
+    if ((j == 0 && o0 != 0) || o1 < o0) set_err(kp.st, ERR_OFFSETS);
+    if (u == kNone) set_err(kp.st, ERR_USER);
+  }
+  if (o1 < o0) return;
+  const uint64_t nb = (o1 - o0) >> 4;
+  if (nb > kp.max_blocks) {
+    if (lane == 0) set_err(kp.st, ERR_BLOCKS);
+    return;
+  }
+  const uint32_t n = (uint32_t)nb;
+  const uint64_t blk0 = o0 >> 4;
+  if (n && blk0 + n > kp.slot_cap) {
+    if (lane == 0) set_err(kp.st, ERR_SLOTCAP);
+    return;
+  }
+  const uint32_t* base = kp.tokens + o0;
+  const int sh = (int)(((uintptr_t)base >> 2) & 3);
+  const uint64_t sig = (POLICY == SOLID_POLICY_USER_ISOLATION) ? sigma_of(kp.seed, u) : 0;
+  const unsigned long long guess =
+      ((unsigned long long)tag_of(kp.epoch, 0) << 32) | (unsigned long long)(j + 1);
+  uint64_t carry = 0;
+  uint32_t bad = 0;
+  for (uint32_t g = 0; g < n; g += 32) {
+    const uint32_t i = g + lane;
+    const bool valid = i < n;
+    uint64_t term = 0;
+    if (valid) {
+      const uint64_t h = hash_block(base + (uint64_t)kBS * i, sh, kp, bad);
+      term = mulmod(addmod(h, sig), kp.mpow[i]);
+    }
+    uint64_t S = addmod(warp_scan_addmod(term, lane), carry);
+    carry = __shfl_sync(0xffffffffu, S, 31);
+    bool created = false;
+    uint64_t pos = 0;
+    if (valid) {
+      pos = scratch_register(kp, key_of(S), created);
+      if (pos != ~0ull) {
+        kp.slot_of_block[blk0 + i] = (uint32_t)pos;
+        atomic_min_u64(&kp.sl[pos].st[0], guess);     // APC first-occurrence guess (P0, tag 0)
+      }
+    }
+    append_created(kp, created, pos, lane, seg);
+  }
+  if (__any_sync(0xffffffffu, bad != 0) && lane == 0) set_err(kp.st, ERR_TOKEN);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K_B: one resolver round t (t >= 1) — the per-request Detector of P:454-459 evaluated against
+// "the state as of this request" reconstructed from round t-1's staged values.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t owner_from(const KParams& kp, const Slot* s,
+                                               unsigned long long ins, uint32_t tagS) {
+  if ((uint32_t)(ins >> 32) == tagS) return s->snap_owner;
+  return kp.users[(uint32_t)ins - 1u];
+}
+
+__device__ __forceinline__ uint64_t iso_key(const KParams& kp, uint64_t blk, uint32_t i,
+                                            uint64_t sig, uint64_t gf) {
+  const uint32_t s = kp.slot_of_block[blk];
+  const uint64_t S = chain_of(kp.sl[s].key);
+  const uint64_t d = submod(kp.gtab[i + 1], gf);   // G[b] - G[f], b = i + 1
+  return key_of(addmod(S, mulmod(sig, d)));
+}
+
+template <int POLICY>
+__global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
+  if (t >= 2 && kp.st->changed[t - 1] == 0) return;     // converged in an earlier round
+  const int lane = threadIdx.x & 31;
+  const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= kp.n) return;
+  const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
+  const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
+  if (o1 < o0) return;
+  const uint64_t nb = (o1 - o0) >> 4;
+  if (nb > kp.max_blocks) return;
+  const uint32_t n = (uint32_t)nb;
+  const uint64_t blk0 = o0 >> 4;
+  if (n && blk0 + n > kp.slot_cap) return;
+  const uint32_t u = kp.users[j];
+  const uint32_t seqp = (uint32_t)(j + 1);
+  const int R = (int)((t - 1) & 1), W = (int)(t & 1);
+  const uint32_t tagR = tag_of(kp.epoch, t - 1), tagW = tag_of(kp.epoch, t),
+                 tagS = tag_of(kp.epoch, kSubSnap);
+  const bool enf = (POLICY == SOLID_POLICY_SOLIDARITY) && (kp.enforce ? kp.enforce[j] != 0 : true);
+
+  // ---- a5: first miss k (warp ballot) and barrier scan f over the Shared chain ----
+  uint32_t k = n;
+  int32_t f = -1;
+  bool carry_flag = false;    // flagged(index g-1) from the previous group
+  for (uint32_t g = 0; g <= n; g += 32) {
+    const uint32_t i = g + lane;
+    const bool valid = i < n;
+    uint32_t s = 0;
+    unsigned long long ins = 0, flg = 0;
+    bool vis = false, fl = false;
+    if (valid) {
+      s = kp.slot_of_block[blk0 + i];
+      const ulonglong2 v = ld_v2u64(&kp.sl[s].st[2 * R]);
+      ins = v.x;
+      flg = v.y;
+      vis = staged_visible(ins, seqp, tagR, tagS);
+      fl = staged_visible(flg, seqp, tagR, tagS);
+    }
+    const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
+    const int L = inv ? __ffs(inv) - 1 : 32;         // first invisible lane in this group
+    if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
+      // lane evaluates the barrier condition for index m = i - 1 (needs flagged(m) and the
+      // owner of the NEXT entry i): stop at m iff flagged(m) and not (i visible and
+      // owned by the requester).
+      bool pf = __shfl_up_sync(0xffffffffu, fl, 1);
+      if (lane == 0) pf = carry_flag;
+      bool cond = false;
+      if (pf && lane <= L && !(g == 0 && lane == 0)) {
+        const bool pass = vis && owner_from(kp, &kp.sl[s], ins, tagS) == u;
+        cond = !pass;
+      }
+      const uint32_t cm = __ballot_sync(0xffffffffu, cond);
+      if (cm) f = (int32_t)(g + (uint32_t)(__ffs(cm) - 1));   // 1-based depth = m + 1 = i
+      carry_flag = __shfl_sync(0xffffffffu, fl, 31);
+    }
+    if (L < 32) {
+      k = g + (uint32_t)L;
+      break;
+    }
+  }
+  if (POLICY == SOLID_POLICY_USER_ISOLATION) f = 0;
+
+  // ---- selective isolation: continue in Iso(u) rooted at S[f] (R3) ----
+  uint32_t r = k, flagd = 0;
+  uint64_t sig = 0, gf = 0;
+  if (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) {
+    sig = sigma_of(kp.seed, u);
+    gf = kp.gtab[f];
+    uint32_t m = n - (uint32_t)f;
+    for (uint32_t g = (uint32_t)f; g < n; g += 32) {
+      const uint32_t i = g + lane;
+      bool vis = false;
+      if (i < n) {
+        const uint64_t key = iso_key(kp, blk0 + i, i, sig, gf);
+        uint64_t pos;
+        if (scratch_find(kp, key, pos))
+          vis = staged_visible(kp.sl[pos].st[2 * R], seqp, tagR, tagS);
+        if (!vis) {
+          uint32_t ow, sr;
+          uint64_t ip;
+          vis = index_find(kp, key, ow, sr, ip);
+        }
+      }
+      const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
+      if (inv) {
+        m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
+        break;
+      }
+    }
+    r = (uint32_t)f + m;
+  } else if (POLICY == SOLID_POLICY_SOLIDARITY && k >= 1) {
+    // flag rule (R2): e_r = K[k] gets flagged iff owner != u and unflagged; applies with
+    // isolation on or off (R11)
+    if (lane == 0) {
+      const uint32_t s = kp.slot_of_block[blk0 + k - 1];
+      const ulonglong2 v = ld_v2u64(&kp.sl[s].st[2 * R]);
+      const bool flagged = staged_visible(v.y, seqp, tagR, tagS);
+      if (!flagged && owner_from(kp, &kp.sl[s], v.x, tagS) != u) {
+        flagd = k;
+        atomic_min_u64(&kp.sl[s].st[2 * W + 1],
+                       ((unsigned long long)tagW << 32) | (unsigned long long)seqp);
+      }
+    }
+    flagd = __shfl_sync(0xffffffffu, flagd, 0);
+  }
+
+  // ---- staged inserts (seq-min scatter); APC / USER_ISOLATION are exact from round 0 ----
+  if (POLICY == SOLID_POLICY_SOLIDARITY) {
+    const unsigned long long mine = ((unsigned long long)tagW << 32) | (unsigned long long)seqp;
+    for (uint32_t g = r; g < n; g += 32) {
+      const uint32_t i = g + lane;
+      bool created = false;
+      uint64_t pos = 0;
+      if (i < n) {
+        if (f >= 1) {
+          pos = scratch_register(kp, iso_key(kp, blk0 + i, i, sig, gf), created);
+        } else {
+          pos = kp.slot_of_block[blk0 + i];
+        }
+        if (pos != ~0ull) atomic_min_u64(&kp.sl[pos].st[2 * W], mine);
+      }
+      append_created(kp, created, pos, lane, seg);
+    }
+  }
+
+  if (lane == 0) {
+    const uint4 d = make_uint4(k, (uint32_t)f, r, flagd);
+    if (POLICY == SOLID_POLICY_SOLIDARITY) {
+      if (t == 1) {
+        kp.st->changed[1] = 1;
+      } else {
+        const uint4 o = kp.dec[j];
+        if (o.x != d.x || o.y != d.y || o.z != d.z || o.w != d.w) kp.st->changed[t] = 1;
+      }
+    }
+    kp.dec[j] = d;
+    const uint32_t kk = (POLICY == SOLID_POLICY_USER_ISOLATION) ? 0u : k;   // no Shared chain
+    solid_result res;
+    res.n_blocks = n;
+    res.shared_hits = kk;
+    res.reused = r;
+    res.divert_at = f;
+    res.flag_depth = flagd;
+    res.bits = (r > 0 ? 1u : 0u) | ((n > 0 && r == n) ? 2u : 0u) | (f >= 0 ? 4u : 0u) |
+               ((f >= 0 && (uint32_t)f < kk) ? 8u : 0u) | (flagd > 0 ? 16u : 0u);
+    kp.out[j] = res;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K_C: commit.  The first inserter of each key (seq-min in the final state) claims an index slot
+// with one 128-bit CAS; the first flagger of a snapshot entry writes its sharer (a6).
+// mode 0 counts new entries (capacity check before any mutation), mode 1 commits.
+// ---------------------------------------------------------------------------------------------
+template <int POLICY>
+__global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mode) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint32_t cnt = 0, fcnt = 0;
+  if (j < kp.n) {
+    const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
+    const uint32_t n = (uint32_t)((o1 - o0) >> 4);
+    const uint64_t blk0 = o0 >> 4;
+    const uint32_t u = kp.users[j];
+    const uint32_t seqp = (uint32_t)(j + 1);
+    const int W = (int)(tf & 1);
+    const uint32_t tag = tag_of(kp.epoch, tf);
+    const uint4 d = kp.dec[j];
+    const uint32_t r = d.z, flagd = d.w;
+    const int32_t f = (int32_t)d.y;
+    uint64_t sig = 0, gf = 0;
+    if (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) {
+      sig = sigma_of(kp.seed, u);
+      gf = kp.gtab[f];
+    }
+    for (uint32_t g = r; g < n; g += 32) {
+      const uint32_t i = g + lane;
+      if (i >= n) break;
+      uint64_t pos;
+      uint64_t key;
+      if (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) {
+        key = iso_key(kp, blk0 + i, i, sig, gf);
+        if (!scratch_find(kp, key, pos)) continue;
+      } else {
+        pos = kp.slot_of_block[blk0 + i];
+        key = kp.sl[pos].key;
+      }
+      const Slot* s = kp.sl + pos;
+      const unsigned long long ins = s->st[2 * W];
+      if ((uint32_t)(ins >> 32) != tag || (uint32_t)ins != seqp) continue;   // not first inserter
+      ++cnt;
+      if (mode == 1) {
+        const unsigned long long fv = s->st[2 * W + 1];
+        const uint32_t sharer =
+            ((uint32_t)(fv >> 32) == tag) ? kp.users[(uint32_t)fv - 1u] : kNone;
+        const ulonglong2 val = make_ulonglong2(key, (unsigned long long)u |
+                                                        ((unsigned long long)sharer << 32));
+        uint64_t p = key & kp.tmask;
+        for (;;) {
+          const ulonglong2 old = atomic_cas128(&kp.tab[p], make_ulonglong2(0ull, 0ull), val);
+          if (old.x == 0 || old.x == key) break;
+          p = (p + 1) & kp.tmask;
+        }
+      }
+    }
+    if (POLICY == SOLID_POLICY_SOLIDARITY && flagd > 0 && lane == 0) {
+      const uint32_t sp = kp.slot_of_block[blk0 + flagd - 1];
+      const Slot* s = kp.sl + sp;
+      const uint32_t tagS = tag_of(kp.epoch, kSubSnap);
+      const unsigned long long fv = s->st[2 * W + 1];
+      if ((uint32_t)(s->st[2 * W] >> 32) == tagS && (uint32_t)(fv >> 32) == tag &&
+          (uint32_t)fv == seqp) {
+        ++fcnt;
+        if (mode == 1) {
+          uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[s->psl].y) + 1;
+          atomicCAS(sharer_word, kNone, u);
+        }
+      }
+    }
+  }
+  // warp reduce the counts, one atomic per warp
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    fcnt += __shfl_xor_sync(0xffffffffu, fcnt, o);
+  }
+  if (lane == 0 && mode == 0 && (cnt | fcnt)) {
+    atomicAdd(&kp.st->new_entries, (unsigned long long)cnt);
+    atomicAdd(&kp.st->new_flags, (unsigned long long)fcnt);
+  }
+}
+
+// Per-batch sums over the results (block-weighted hit rate).
+__global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t n,
+                                               DevStatus* st) {
+  unsigned long long a[6] = {0, 0, 0, 0, 0, 0};
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const solid_result r = out[j];
+    a[0] += r.n_blocks;
+    a[1] += r.reused;
+    a[2] += (r.bits >> 4) & 1;
+    a[3] += (r.bits >> 2) & 1;
+    a[4] += (r.bits >> 3) & 1;
+    a[5] += 1;
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    for (int o = 16; o; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+    if ((threadIdx.x & 31) == 0 && a[q]) atomicAdd(&st->sums[q], a[q]);
+  }
+}
+
+// Clear the scratch keys registered by this batch.
+__global__ void __launch_bounds__(256) k_cleanup(Slot* sl, const uint32_t* seg_cnt,
+                                                 const uint32_t* seg_list, uint32_t seg_cap) {
+  const uint32_t seg = blockIdx.y;
+  const uint32_t c = min(seg_cnt[seg], seg_cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
+    sl[seg_list[(uint64_t)seg * seg_cap + i]].key = 0ull;
+}
+
+__global__ void k_init_slots(Slot* sl, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    Slot s;
+    s.key = 0;
+    s.snap_owner = kNone;
+    s.snap_sharer = kNone;
+    s.psl = kNone;
+    s.pad[0] = s.pad[1] = s.pad[2] = 0;
+    s.st[0] = s.st[1] = s.st[2] = s.st[3] = ~0ull;
+    sl[i] = s;
+  }
+}
+
+}  // namespace solid
+
+// =============================================================================================
+// Host runtime
+// =============================================================================================
+using namespace solid;
+
+struct solid_ctx {
+  solid_config cfg{};
+  int dev = 0;
+  bool poisoned = false;
+  bool pending = false;
+  std::string err;
+  // index
+  ulonglong2* tab = nullptr;
+  uint64_t tcap = 0;
+  uint64_t live = 0;
+  ulonglong2* tab_ckpt = nullptr;
+  uint64_t live_ckpt = 0;
+  // scratch
+  Slot* sl = nullptr;
+  uint64_t scap = 0;
+  uint32_t* slot_of_block = nullptr;
+  uint64_t slot_cap = 0;
+  uint4* dec = nullptr;
+  uint32_t* seg_cnt = nullptr;
+  uint32_t* seg_list = nullptr;
+  uint32_t seg_cap = 0;
+  DevStatus* st = nullptr;
+  DevStatus* st_host = nullptr;   // pinned mirror
+  unsigned long long* mpow = nullptr;
+  unsigned long long* gtab = nullptr;
+  uint32_t klo[kBS], khi[kBS];
+  uint32_t epoch = 0;
+  // pending batch
+  KParams kp{};
+  uint32_t tf = 0;
+  uint32_t rounds = 0;
+  cudaStream_t stream = nullptr;
+  // host-buffer admission staging
+  uint32_t* h_tokens = nullptr;
+  uint64_t* h_offsets = nullptr;
+  uint32_t* h_users = nullptr;
+  uint8_t* h_enforce = nullptr;
+  solid_result* h_out = nullptr;
+  // stats
+  solid_stats_t stats{};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  uint64_t launches = 0;
+  uint32_t seg_host[kNSeg];
+  bool ev_valid = false;
+};
+
+static uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+static solid_status fail(solid_ctx* c, solid_status s, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (s == SOLID_ERR_CUDA) c->poisoned = true;
+  }
+  return s;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, SOLID_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+extern "C" uint32_t solid_abi_version(void) { return SOLID_ABI_VERSION; }
+
+extern "C" const char* solid_last_error(const solid_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : "null context";
+}
+
+static void free_all(solid_ctx* c) {
+  cudaFree(c->tab);
+  cudaFree(c->tab_ckpt);
+  cudaFree(c->sl);
+  cudaFree(c->slot_of_block);
+  cudaFree(c->dec);
+  cudaFree(c->seg_cnt);
+  cudaFree(c->seg_list);
+  cudaFree(c->st);
+  cudaFree(c->mpow);
+  cudaFree(c->gtab);
+  cudaFree(c->h_tokens);
+  cudaFree(c->h_offsets);
+  cudaFree(c->h_users);
+  cudaFree(c->h_enforce);
+  cudaFree(c->h_out);
+  if (c->st_host) cudaFreeHost(c->st_host);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+}
+
+extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
+  solid_ctx* ctx = nullptr;
+  if (!cfg || !out) return SOLID_ERR_INVALID;
+  *out = nullptr;
+  if (cfg->block_size != kBS || cfg->max_blocks == 0 || cfg->max_blocks > (1u << 24) ||
+      cfg->capacity_blocks == 0 || cfg->max_batch_requests == 0 ||
+      cfg->max_batch_requests >= 0xFFFFFFF0ull || cfg->policy < 0 || cfg->policy > 2)
+    return SOLID_ERR_INVALID;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
+    return SOLID_ERR_INVALID;
+  ctx = new solid_ctx();
+  ctx->cfg = *cfg;
+  ctx->dev = cfg->device;
+  CK(cudaSetDevice(ctx->dev));
+  ctx->tcap = next_pow2(std::max<uint64_t>(2 * cfg->capacity_blocks, 1024));
+  ctx->slot_cap = cfg->max_batch_tokens / kBS + 1;
+  ctx->scap = next_pow2(std::max<uint64_t>(4 * ctx->slot_cap, 4096));
+  if (ctx->tcap > (1ull << 32) || ctx->scap > (1ull << 32)) {   // slot indices are 32-bit
+    delete ctx;
+    return SOLID_ERR_INVALID;
+  }
+  ctx->seg_cap = (uint32_t)std::min<uint64_t>(2 * ctx->scap / kNSeg + 1024, 0xFFFFFFF0ull);
+  const uint64_t mb = cfg->max_blocks;
+  auto alloc = [&](void** p, size_t bytes) -> bool { return cudaMalloc(p, bytes) == cudaSuccess; };
+  bool ok = alloc((void**)&ctx->tab, ctx->tcap * sizeof(ulonglong2)) &&
+            alloc((void**)&ctx->sl, ctx->scap * sizeof(Slot)) &&
+            alloc((void**)&ctx->slot_of_block, ctx->slot_cap * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->dec, cfg->max_batch_requests * sizeof(uint4)) &&
+            alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->seg_list, (uint64_t)kNSeg * ctx->seg_cap * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->st, sizeof(DevStatus)) &&
+            alloc((void**)&ctx->mpow, mb * sizeof(unsigned long long)) &&
+            alloc((void**)&ctx->gtab, (mb + 1) * sizeof(unsigned long long)) &&
+            cudaMallocHost((void**)&ctx->st_host, sizeof(DevStatus)) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    free_all(ctx);
+    delete ctx;
+    return SOLID_ERR_OOM;
+  }
+  // H-def v2 constants, computed by this library's own host code.
+  const uint64_t B = (1ull << 32) + splitmix64(cfg->hash_seed) % (kP - (1ull << 33));
+  uint64_t pw = 1;
+  for (uint32_t i = 0; i < kBS; ++i) {
+    ctx->klo[i] = (uint32_t)pw;
+    ctx->khi[i] = (uint32_t)(pw >> 32);
+    pw = mulmod_host(pw, B);
+  }
+  const uint64_t M = pw;
+  std::vector<unsigned long long> mp(mb), g(mb + 1);
+  uint64_t x = 1;
+  g[0] = 0;
+  for (uint64_t i = 0; i < mb; ++i) {
+    mp[i] = x;
+    g[i + 1] = addmod(g[i], x);
+    x = mulmod_host(x, M);
+  }
+  CK(cudaMemcpy(ctx->mpow, mp.data(), mb * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->gtab, g.data(), (mb + 1) * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemset(ctx->tab, 0, ctx->tcap * sizeof(ulonglong2)));
+  k_init_slots<<<4096, 256>>>(ctx->sl, ctx->scap);
+  CK(cudaGetLastError());
+  CK(cudaMemset(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t)));
+  CK(cudaMemset(ctx->st, 0, sizeof(DevStatus)));
+  for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+  CK(cudaDeviceSynchronize());
+  *out = ctx;
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_destroy(solid_ctx* ctx) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  cudaSetDevice(ctx->dev);
+  cudaDeviceSynchronize();
+  free_all(ctx);
+  delete ctx;
+  return SOLID_OK;
+}
+
+static unsigned grid_for_warps(uint64_t warps) {
+  return (unsigned)((warps * 32 + 255) / 256);
+}
+
+static void launch_eval(solid_ctx* c, uint32_t t, cudaStream_t s) {
+  const unsigned grid = grid_for_warps(c->kp.n);
+  switch (c->cfg.policy) {
+    case SOLID_POLICY_APC: k_eval<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(c->kp, t); break;
+    case SOLID_POLICY_USER_ISOLATION:
+      k_eval<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(c->kp, t); break;
+    default: k_eval<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(c->kp, t); break;
+  }
+}
+
+static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
+  const unsigned grid = grid_for_warps(c->kp.n);
+  switch (c->cfg.policy) {
+    case SOLID_POLICY_APC: k_commit<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(c->kp, c->tf, mode); break;
+    case SOLID_POLICY_USER_ISOLATION:
+      k_commit<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(c->kp, c->tf, mode); break;
+    default: k_commit<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(c->kp, c->tf, mode); break;
+  }
+}
+
+static solid_status cleanup_scratch(solid_ctx* ctx, cudaStream_t s) {
+  k_cleanup<<<dim3(8, kNSeg), 256, 0, s>>>(ctx->sl, ctx->seg_cnt, ctx->seg_list, ctx->seg_cap);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t), s));
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b, solid_result* out,
+                                           void* stream) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
+  if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "lookup_batch twice without insert_batch");
+  if (!b || (b->n_requests && (!b->tokens || !b->offsets || !b->users || !out)) || !b->offsets)
+    return fail(ctx, SOLID_ERR_INVALID, "null batch pointer");
+  if (b->n_requests > ctx->cfg.max_batch_requests)
+    return fail(ctx, SOLID_ERR_INVALID, "n_requests > max_batch_requests");
+  if (((uintptr_t)b->tokens & 3) != 0) return fail(ctx, SOLID_ERR_INVALID, "tokens not 4-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(ctx->dev));
+  ctx->stream = s;
+  if (++ctx->epoch > kMaxEpoch) {     // tag space exhausted: re-initialise the staged states
+    k_init_slots<<<4096, 256, 0, s>>>(ctx->sl, ctx->scap);
+    CK(cudaGetLastError());
+    ctx->epoch = 1;
+  }
+  KParams& kp = ctx->kp;
+  memcpy(kp.klo, ctx->klo, sizeof(kp.klo));
+  memcpy(kp.khi, ctx->khi, sizeof(kp.khi));
+  kp.mpow = ctx->mpow;
+  kp.gtab = ctx->gtab;
+  kp.seed = ctx->cfg.hash_seed;
+  kp.tokens = b->tokens;
+  kp.offsets = b->offsets;
+  kp.users = b->users;
+  kp.enforce = b->enforce;
+  kp.n = b->n_requests;
+  kp.max_blocks = ctx->cfg.max_blocks;
+  kp.epoch = ctx->epoch;
+  kp.sl = ctx->sl;
+  kp.smask = ctx->scap - 1;
+  kp.tab = ctx->tab;
+  kp.tmask = ctx->tcap - 1;
+  kp.slot_of_block = ctx->slot_of_block;
+  kp.slot_cap = ctx->slot_cap;
+  kp.dec = ctx->dec;
+  kp.out = out;
+  kp.seg_cnt = ctx->seg_cnt;
+  kp.seg_list = ctx->seg_list;
+  kp.seg_cap = ctx->seg_cap;
+  kp.st = ctx->st;
+  CK(cudaMemsetAsync(ctx->st, 0, sizeof(DevStatus), s));
+  CK(cudaEventRecord(ctx->ev[0], s));
+  const uint64_t n = b->n_requests;
+  uint32_t rounds = 0;
+  if (n) {
+    const unsigned grid = grid_for_warps(n);
+    switch (ctx->cfg.policy) {
+      case SOLID_POLICY_APC: k_hash_register<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(kp); break;
+      case SOLID_POLICY_USER_ISOLATION:
+        k_hash_register<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(kp); break;
+      default: k_hash_register<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(kp); break;
+    }
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(ctx->ev[1], s));
+  ctx->launches = n ? 1 : 0;
+  if (n && ctx->cfg.policy != SOLID_POLICY_SOLIDARITY) {
+    CK(cudaEventRecord(ctx->ev[4], s));
+    launch_eval(ctx, 1, s);      // exact in one pass: round-0 first occurrences are final
+    CK(cudaEventRecord(ctx->ev[5], s));
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    ctx->tf = 0;
+    rounds = 1;
+    CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  } else if (n) {
+    // Jacobi rounds until no decision changes.  Rounds are enqueued ahead in
+    // chunks; a round whose predecessor saw no change exits at once.
+    uint32_t t = 1, conv = 0, chunk = 4;
+    while (!conv) {
+      for (uint32_t q = 0; q < chunk && t <= kMaxRounds; ++q, ++t) {
+        if (t == 1) CK(cudaEventRecord(ctx->ev[4], s));
+        launch_eval(ctx, t, s);
+        if (t == 1) CK(cudaEventRecord(ctx->ev[5], s));
+        ctx->launches += 1;
+      }
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (ctx->st_host->err) break;
+      for (uint32_t q = 2; q < t; ++q)
+        if (ctx->st_host->changed[q] == 0) {
+          conv = q;
+          break;
+        }
+      if (!conv && t > kMaxRounds) {
+        cleanup_scratch(ctx, s);
+        return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
+      }
+      chunk = std::min<uint32_t>(chunk * 2, 64);
+    }
+    ctx->tf = conv;
+    rounds = conv;
+  } else {
+    CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  CK(cudaEventRecord(ctx->ev[2], s));
+  if (ctx->st_host->err) {
+    const uint32_t e = ctx->st_host->err;
+    solid_status rc = cleanup_scratch(ctx, s);
+    if (rc != SOLID_OK) return rc;
+    CK(cudaStreamSynchronize(s));
+    std::string m = "invalid batch:";
+    if (e & ERR_OFFSETS) m += " offsets";
+    if (e & ERR_TOKEN) m += " token>=2^20";
+    if (e & ERR_USER) m += " user==NONE";
+    if (e & ERR_BLOCKS) m += " request>max_blocks";
+    if (e & ERR_SLOTCAP) m += " tokens>max_batch_tokens";
+    if (e & ERR_SCRATCH) return fail(ctx, SOLID_ERR_CAPACITY, "batch scratch overflow");
+    return fail(ctx, SOLID_ERR_INVALID, m);
+  }
+  ctx->rounds = rounds;
+  ctx->pending = true;
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
+  if (!ctx->pending) return fail(ctx, SOLID_ERR_STATE, "insert_batch without a pending lookup");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(ctx->dev));
+  const uint64_t n = ctx->kp.n;
+  if (n) {
+    launch_commit(ctx, 0, s);
+    CK(cudaGetLastError());
+    ctx->launches += 1;
+    CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t add = ctx->st_host->new_entries;
+    if (ctx->live + add > ctx->cfg.capacity_blocks) {
+      solid_status rc = cleanup_scratch(ctx, s);
+      ctx->pending = false;
+      if (rc != SOLID_OK) return rc;
+      return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9)");
+    }
+    launch_commit(ctx, 1, s);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+    k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(ctx->kp.out, n, ctx->st);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(ctx->ev[3], s));
+  CK(cudaMemcpyAsync(ctx->seg_host, ctx->seg_cnt, sizeof(ctx->seg_host), cudaMemcpyDeviceToHost, s));
+  solid_status rc = cleanup_scratch(ctx, s);
+  if (rc != SOLID_OK) return rc;
+  ctx->launches += 1;
+  CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const DevStatus& h = *ctx->st_host;
+  solid_stats_t& S = ctx->stats;
+  S.batches += 1;
+  S.requests += n;
+  S.blocks += h.sums[0];
+  S.reused_blocks += h.sums[1];
+  S.flagged += h.sums[2];
+  S.diverted += h.sums[3];
+  S.truncated += h.sums[4];
+  S.inserted += h.new_entries;
+  ctx->live += h.new_entries;
+  S.live_entries = ctx->live;
+  S.last_rounds = ctx->rounds;
+  uint64_t distinct = 0;
+  for (int q = 0; q < kNSeg; ++q) distinct += ctx->seg_host[q];
+  S.last_distinct_keys = (uint32_t)std::min<uint64_t>(distinct, 0xFFFFFFFFull);
+  S.last_kernel_launches = ctx->launches;
+  S.last_requests = n;
+  S.last_blocks = h.sums[0];
+  S.last_inserted = h.new_entries;
+  S.last_flagged = h.sums[2];
+  S.algorithmic_bytes = 64ull * h.sums[0] + 37ull * n + 16ull * h.new_entries + 4ull * h.new_flags;
+  ctx->ev_valid = true;
+  ctx->pending = false;
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
+                                         solid_result* out_host, void* stream) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
+  if (!hb || !hb->offsets || (hb->n_requests && (!hb->tokens || !hb->users || !out_host)))
+    return fail(ctx, SOLID_ERR_INVALID, "null batch pointer");
+  const uint64_t n = hb->n_requests;
+  if (n > ctx->cfg.max_batch_requests)
+    return fail(ctx, SOLID_ERR_INVALID, "n_requests > max_batch_requests");
+  const uint64_t T = hb->offsets[n];
+  if (T > ctx->cfg.max_batch_tokens) return fail(ctx, SOLID_ERR_INVALID, "tokens > max_batch_tokens");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!ctx->h_tokens) {
+    const uint64_t R = ctx->cfg.max_batch_requests;
+    CK(cudaMalloc(&ctx->h_tokens, (ctx->cfg.max_batch_tokens + 4) * 4));
+    CK(cudaMalloc(&ctx->h_offsets, (R + 1) * 8));
+    CK(cudaMalloc(&ctx->h_users, R * 4 + 4));
+    CK(cudaMalloc(&ctx->h_enforce, R + 1));
+    CK(cudaMalloc(&ctx->h_out, R * sizeof(solid_result) + 32));
+  }
+  if (T) CK(cudaMemcpyAsync(ctx->h_tokens, hb->tokens, T * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->h_offsets, hb->offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+  if (n) CK(cudaMemcpyAsync(ctx->h_users, hb->users, n * 4, cudaMemcpyHostToDevice, s));
+  if (n && hb->enforce) CK(cudaMemcpyAsync(ctx->h_enforce, hb->enforce, n, cudaMemcpyHostToDevice, s));
+  solid_batch db;
+  db.n_requests = n;
+  db.tokens = ctx->h_tokens;
+  db.offsets = ctx->h_offsets;
+  db.users = ctx->h_users;
+  db.enforce = hb->enforce ? ctx->h_enforce : nullptr;
+  solid_status rc = solid_lookup_batch(ctx, &db, ctx->h_out, stream);
+  if (rc != SOLID_OK) return rc;
+  rc = solid_insert_batch(ctx, stream);
+  if (rc != SOLID_OK) return rc;
+  if (n) CK(cudaMemcpyAsync(out_host, ctx->h_out, n * sizeof(solid_result), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out) {
+  if (!ctx || !out) return SOLID_ERR_INVALID;
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->ev_valid) {
+    CK(cudaEventSynchronize(ctx->ev[3]));
+    cudaEventElapsedTime(&ctx->stats.ms_hash, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&ctx->stats.ms_resolve, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&ctx->stats.ms_commit, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&ctx->stats.ms_hash_kernel, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&ctx->stats.ms_round_first, ctx->ev[4], ctx->ev[5]);
+  }
+  *out = ctx->stats;
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64_t cap,
+                                   uint64_t* n_out) {
+  if (!ctx || !n_out || (cap && !host_out)) return SOLID_ERR_INVALID;
+  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<ulonglong2> h(ctx->tcap);
+  CK(cudaMemcpy(h.data(), ctx->tab, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToHost));
+  std::vector<solid_entry> v;
+  v.reserve(ctx->live);
+  for (const auto& e : h)
+    if (e.x) v.push_back(solid_entry{e.x, (uint32_t)e.y, (uint32_t)(e.y >> 32)});
+  std::sort(v.begin(), v.end(), [](const solid_entry& a, const solid_entry& b) { return a.key < b.key; });
+  *n_out = v.size();
+  const uint64_t m = std::min<uint64_t>(cap, v.size());
+  if (m) memcpy(host_out, v.data(), m * sizeof(solid_entry));
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_reset(solid_ctx* ctx) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemset(ctx->tab, 0, ctx->tcap * sizeof(ulonglong2)));
+  if (ctx->pending || ctx->poisoned) {
+    k_init_slots<<<4096, 256>>>(ctx->sl, ctx->scap);
+    CK(cudaGetLastError());
+    CK(cudaMemset(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t)));
+  }
+  CK(cudaDeviceSynchronize());
+  ctx->live = 0;
+  ctx->pending = false;
+  ctx->poisoned = false;
+  ctx->stats = solid_stats_t{};
+  ctx->ev_valid = false;
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_checkpoint(solid_ctx* ctx) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "checkpoint with a pending batch");
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+  if (!ctx->tab_ckpt) CK(cudaMalloc(&ctx->tab_ckpt, ctx->tcap * sizeof(ulonglong2)));
+  CK(cudaMemcpy(ctx->tab_ckpt, ctx->tab, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToDevice));
+  ctx->live_ckpt = ctx->live;
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_restore(solid_ctx* ctx) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  if (!ctx->tab_ckpt) return fail(ctx, SOLID_ERR_STATE, "restore without checkpoint");
+  if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "restore with a pending batch");
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(ctx->tab, ctx->tab_ckpt, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToDevice));
+  ctx->live = ctx->live_ckpt;
+  return SOLID_OK;
+}
