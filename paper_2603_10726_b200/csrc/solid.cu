@@ -2,17 +2,23 @@
 //
 // Hot path of one batch:
 //   K_A  k_hash_register   tokens -> per-block hash (a2) -> chained-prefix scan (a3) -> key ->
-//                          register in the batch scratch table (a4; probes the index once per
+//                          register in the batch key table (a4; the index is probed once per
 //                          distinct key) -> APC first-occurrence guess
 //   K_B  k_eval<POLICY>    per-request first miss (a5, warp ballot), barrier scan, isolated walk,
-//                          flag decision, seq-min scatter of staged inserts/flags  — repeated
+//                          flag decision, seq-min scatter of staged inserts/flags — repeated
 //                          (Jacobi rounds) until no decision changes = the sequential answer (R1)
-//   K_C  k_commit          128-bit CAS claims {key, owner, sharer} + sharer writes (a6)
-//   K_D  k_stats / k_cleanup
+//   K_C  k_commit          128-bit CAS claims {key, owner, sharer} + sharer writes (a6);
+//                          the same kernel rolls a batch back exactly on capacity overflow
+//   K_D  k_stats           per-batch sums
 //
-// Sequence tags.  Every staged value is a u64 (tag << 32 | seq') with tag = ~(epoch*4096 + sub),
+// Batch key table ("scratch"): open addressing over 16-byte slots {key ^ salt(E), id | E << 32}
+// written by one 128-bit CAS.  A slot is live only for the batch epoch E that wrote it, so the
+// table is never cleared.  Each distinct key gets a dense id; its staged state lives in Hot[id]
+// (32 bytes = one sector) and its index snapshot in Cold[id].
+//
+// Sequence tags.  Every staged value is a u64 (tag << 32 | seq') with tag = ~(E*4096 + sub),
 // seq' = batch position + 1, sub = 0 (round-0 guess), t (round t), 4095 (index snapshot).  atomicMin
-// keeps the EARLIEST request of the newest tag, so stale rounds/batches never need clearing.
+// keeps the EARLIEST request of the newest tag, so stale rounds and batches never need clearing.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,7 +33,7 @@
 
 namespace solid {
 
-constexpr int kNSeg = 128;            // created-list segments (spread the append atomics)
+constexpr int kNSeg = 128;            // id-allocation segments (spread the allocation atomics)
 constexpr uint32_t kSubSnap = 4095;
 constexpr uint32_t kMaxRounds = 4093;
 constexpr uint32_t kMaxEpoch = (0xFFFFFFFFu / 4096u) - 1;
@@ -36,22 +42,24 @@ enum : uint32_t {
   ERR_OFFSETS = 1, ERR_TOKEN = 2, ERR_USER = 4, ERR_BLOCKS = 8, ERR_SCRATCH = 16, ERR_SLOTCAP = 32
 };
 
-// 64-byte scratch slot: one key of the batch (Shared or isolated) and its staged state.
-struct __align__(64) Slot {
-  unsigned long long key;          // 0 = empty
-  uint32_t snap_owner;             // owner in the index at batch start, kNone = absent
-  uint32_t snap_sharer;            // sharer in the index at batch start
-  uint32_t psl;                    // index slot of the snapshot entry
-  uint32_t pad[3];
-  unsigned long long st[4];        // ping-pong: [0]=P0.ins [1]=P0.flg [2]=P1.ins [3]=P1.flg
+struct __align__(32) Hot {            // staged state of one key (ping-pong by round parity)
+  unsigned long long ins[2];          // first inserter: tag << 32 | seq'
+  unsigned long long flg[2];          // first flagger:  tag << 32 | seq'
 };
-static_assert(sizeof(Slot) == 64, "slot layout");
+struct Cold {                         // the key and its index snapshot at batch start
+  unsigned long long key;
+  uint32_t snap_owner;                // kNone = absent from the index
+  uint32_t snap_sharer;
+  uint32_t psl;                       // index slot (snapshot entry, or the slot claimed at commit)
+  uint32_t pad;
+};
+static_assert(sizeof(Hot) == 32 && sizeof(Cold) == 24, "layout");
 
 struct DevStatus {
   uint32_t err;
   uint32_t pad;
-  unsigned long long new_entries;        // k_commit count mode
-  unsigned long long new_flags;          // flags on index (snapshot) entries
+  unsigned long long new_entries;        // entries claimed by k_commit
+  unsigned long long new_flags;          // sharer writes on index (snapshot) entries
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
   uint32_t changed[kMaxRounds + 2];
 };
@@ -68,16 +76,19 @@ struct KParams {
   uint64_t n;
   uint32_t max_blocks;
   uint32_t epoch;
-  Slot* sl;
+  unsigned long long salt;         // per-epoch key salt of the batch key table
+  ulonglong2* stab;                // batch key table
   uint64_t smask;
-  ulonglong2* tab;
+  Hot* hot;
+  Cold* cold;
+  ulonglong2* tab;                 // the index {key, owner | sharer << 32}
   uint64_t tmask;
-  uint32_t* slot_of_block;
+  uint32_t* id_of_block;           // per block: id of its Shared (USER_ISOLATION: U) key
+  uint32_t* iso_id;                // per block: id of its isolated key (valid for dec.f)
   uint64_t slot_cap;
   uint4* dec;
   solid_result* out;
   uint32_t* seg_cnt;
-  uint32_t* seg_list;
   uint32_t seg_cap;
   DevStatus* st;
 };
@@ -95,9 +106,17 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t* p) {
   return r;
 }
 
-__device__ __forceinline__ ulonglong2 ld_v2u64(const void* p) {
+// Weak (L1-cacheable) loads kept in program order.  Used where a stale value is safe: table
+// slots only move stale -> live within a batch, staged values only decrease, and L1 is
+// invalidated at every kernel launch.
+__device__ __forceinline__ ulonglong2 ldw128(const void* p) {
   ulonglong2 r;
   asm volatile("ld.global.v2.u64 {%0,%1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ldw64(const void* p) {
+  unsigned long long r;
+  asm volatile("ld.global.u64 %0, [%1];" : "=l"(r) : "l"(p));
   return r;
 }
 
@@ -119,65 +138,58 @@ __device__ __forceinline__ ulonglong2 atomic_cas128(ulonglong2* addr, ulonglong2
 
 __device__ __forceinline__ void atomic_min_u64(unsigned long long* a, unsigned long long v) {
   // read-before-atomic: values only ever decrease, so a stale read is >= the true value.
-  if (*(volatile unsigned long long*)a > v) atomicMin(a, v);
+  if (ldw64(a) > v) atomicMin(a, v);
+}
+
+// Is a staged value (tag << 32 | seq') visible to request seq' = seqp, reading round tag `tagR`?
+__device__ __forceinline__ bool staged_visible(unsigned long long v, uint32_t seqp, uint32_t tagR,
+                                               uint32_t tagS) {
+  const uint32_t tg = (uint32_t)(v >> 32);
+  return tg == tagS || (tg == tagR && (uint32_t)v < seqp);
 }
 
 // ---------------------------------------------------------------------------------------------
-// a2: per-block hash h = sum_i (tok_i + 1) * K_i mod p over one 16-token block.
-// `sh` = (address / 4) mod 4 is warp-uniform (all blocks of a request share it).
+// a2: per-block hash h = sum_i (tok_i + 1) * K_i mod p over one 16-token block.  SH = (address/4)
+// mod 4 is warp-uniform (all blocks of a request share it); misaligned blocks read the aligned
+// 20-word window and select.
 // ---------------------------------------------------------------------------------------------
 template <int SH>
-__device__ __forceinline__ uint64_t hash16(const uint32_t* p, const KParams& kp, uint32_t& bad) {
-  uint32_t t[16];
-  if (SH == 0) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 v = ldg_v4(p + 4 * q);
-      t[4 * q] = v.x; t[4 * q + 1] = v.y; t[4 * q + 2] = v.z; t[4 * q + 3] = v.w;
-    }
-  } else {
-    uint32_t w[20];
+struct BlockWords {
+  static constexpr int W = SH ? 20 : 16;
+  uint32_t w[W];
+  __device__ __forceinline__ void load(const uint32_t* p) {
     const uint32_t* a = p - SH;
 #pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      uint4 v = ldg_v4(a + 4 * q);
+    for (int q = 0; q < W / 4; ++q) {
+      const uint4 v = ldg_v4(a + 4 * q);
       w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
     }
+  }
+  __device__ __forceinline__ uint64_t hash(const KParams& kp, uint32_t& bad) const {
+    uint64_t lo = 0, hi = 0;
+    uint32_t orv = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) t[i] = w[i + SH];
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t t = w[i + SH];
+      orv |= t;
+      const uint32_t x = t + 1u;
+      lo += (uint64_t)x * kp.klo[i];
+      hi += (uint64_t)x * kp.khi[i];
+    }
+    bad |= orv >> 20;
+    // lo + hi*2^32 mod p, with hi*2^32 = (hi mod 2^29)*2^32 + (hi >> 29)*2^61 == ... + (hi >> 29)
+    return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
   }
-  uint64_t lo = 0, hi = 0;
-  uint32_t orv = 0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    orv |= t[i];
-    const uint32_t x = t[i] + 1u;
-    lo += (uint64_t)x * kp.klo[i];
-    hi += (uint64_t)x * kp.khi[i];
-  }
-  bad |= orv >> 20;
-  // lo + hi*2^32 mod p, with hi*2^32 = (hi mod 2^29)*2^32 + (hi >> 29)*2^61 == ... + (hi >> 29)
-  return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
-}
-
-__device__ __forceinline__ uint64_t hash_block(const uint32_t* p, int sh, const KParams& kp,
-                                               uint32_t& bad) {
-  switch (sh) {
-    case 0: return hash16<0>(p, kp, bad);
-    case 1: return hash16<1>(p, kp, bad);
-    case 2: return hash16<2>(p, kp, bad);
-    default: return hash16<3>(p, kp, bad);
-  }
-}
+};
 
 // ---------------------------------------------------------------------------------------------
-// Index (persistent table) probe: linear probing over 16-byte slots {key, owner | sharer << 32}.
+// Index probe: linear probing over 16-byte slots {key, owner | sharer << 32}; 0 = empty.
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ bool index_find(const KParams& kp, uint64_t key, uint32_t& owner,
                                            uint32_t& sharer, uint64_t& pos) {
   pos = key & kp.tmask;
   for (;;) {
-    ulonglong2 e = ld_v2u64(&kp.tab[pos]);
+    const ulonglong2 e = ldw128(&kp.tab[pos]);
     if (e.x == key) {
       owner = (uint32_t)e.y;
       sharer = (uint32_t)(e.y >> 32);
@@ -192,90 +204,148 @@ __device__ __forceinline__ uint64_t scratch_home(uint64_t key, uint64_t mask) {
   return (key ^ (key >> 29)) & mask;
 }
 
-// First touch of a scratch slot in this batch: record the index snapshot of the key and seed
-// both ping-pong states with it (snapshot tag = the smallest tag of the batch).
-__device__ void init_slot(const KParams& kp, Slot* s, uint64_t key) {
+// The creator of an id records the key and its index snapshot, and seeds both ping-pong states
+// with it (the snapshot tag is the smallest tag of the batch, so it is never displaced).
+__device__ void init_id(const KParams& kp, uint32_t id, uint64_t key) {
   uint32_t owner = kNone, sharer = kNone;
   uint64_t ipos = 0;
   const bool present = index_find(kp, key, owner, sharer, ipos);
-  s->snap_owner = present ? owner : kNone;
-  s->snap_sharer = present ? sharer : kNone;
-  s->psl = present ? (uint32_t)ipos : kNone;
+  Cold c;
+  c.key = key;
+  c.snap_owner = present ? owner : kNone;
+  c.snap_sharer = present ? sharer : kNone;
+  c.psl = present ? (uint32_t)ipos : kNone;
+  c.pad = 0;
+  kp.cold[id] = c;
   if (present) {
+    Hot* h = kp.hot + id;
     const unsigned long long v = (unsigned long long)tag_of(kp.epoch, kSubSnap) << 32;
-    atomicMin(&s->st[0], v);
-    atomicMin(&s->st[2], v);
+    atomicMin(&h->ins[0], v);
+    atomicMin(&h->ins[1], v);
     if (sharer != kNone) {
-      atomicMin(&s->st[1], v);
-      atomicMin(&s->st[3], v);
+      atomicMin(&h->flg[0], v);
+      atomicMin(&h->flg[1], v);
     }
   }
 }
 
-// Find-or-insert `key` in the scratch table.  Returns the slot index; `created` is set for the
-// thread that claimed it.  Keys are never removed during a batch (k_cleanup clears them after).
-__device__ __forceinline__ uint64_t scratch_register(const KParams& kp, uint64_t key,
-                                                     bool& created) {
+// Warp-cooperative find-or-insert of one key per active lane.  Returns the key's id (0 only on
+// scratch overflow); `created` is set for the lane whose CAS published the key.  New ids are
+// allocated with one atomic per warp and probe step (segment `seg`).
+__device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool active, uint64_t key,
+                                                     uint32_t seg, int lane, bool& created) {
+  const unsigned long long kx = key ^ kp.salt;
+  const uint32_t E = kp.epoch;
   uint64_t pos = scratch_home(key, kp.smask);
+  uint32_t id = 0;
+  bool done = !active;
+  bool have_e = false;           // e holds the slot's current value from a failed CAS
+  ulonglong2 e = make_ulonglong2(0, 0);
+  created = false;
   for (uint64_t probes = 0;; ++probes) {
-    Slot* s = kp.sl + pos;
-    unsigned long long k = *(volatile unsigned long long*)&s->key;
-    if (k == key) return pos;
-    if (k == 0) {
-      unsigned long long old = atomicCAS(&s->key, 0ull, (unsigned long long)key);
-      if (old == 0) {
-        created = true;
-        init_slot(kp, s, key);
-        return pos;
+    bool want = false;
+    if (!done) {
+      if (!have_e) e = ldw128(&kp.stab[pos]);
+      have_e = false;
+      if ((uint32_t)(e.y >> 32) == E) {            // live in this batch
+        if (e.x == kx) {
+          id = (uint32_t)e.y;
+          done = true;
+        } else {
+          pos = (pos + 1) & kp.smask;
+        }
+      } else {
+        want = true;                                // stale or never used: claim it
       }
-      if (old == key) return pos;
     }
-    pos = (pos + 1) & kp.smask;
+    const uint32_t wm = __ballot_sync(0xffffffffu, want);
+    if (wm) {
+      uint32_t base = 0;
+      if (lane == __ffs(wm) - 1) base = atomicAdd(&kp.seg_cnt[seg], (uint32_t)__popc(wm));
+      base = __shfl_sync(0xffffffffu, base, __ffs(wm) - 1);
+      if (want) {
+        const uint32_t idx = base + __popc(wm & ((1u << lane) - 1u));
+        if (idx >= kp.seg_cap) {
+          set_err(kp.st, ERR_SCRATCH);
+          done = true;
+        } else {
+          const uint32_t mine = seg * kp.seg_cap + idx + 1;
+          const ulonglong2 nv =
+              make_ulonglong2(kx, (unsigned long long)mine | ((unsigned long long)E << 32));
+          const ulonglong2 old = atomic_cas128(&kp.stab[pos], e, nv);
+          if (old.x == e.x && old.y == e.y) {
+            id = mine;
+            created = true;
+            done = true;
+            init_id(kp, id, key);
+          } else {
+            e = old;                                // authoritative current value: re-examine
+            have_e = true;                          // without trusting a possibly stale L1 line
+          }
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
     if (probes > kp.smask) {
-      set_err(kp.st, ERR_SCRATCH);
-      return ~0ull;
+      if (!done) set_err(kp.st, ERR_SCRATCH);
+      break;
     }
   }
+  return id;
 }
 
-__device__ __forceinline__ bool scratch_find(const KParams& kp, uint64_t key, uint64_t& pos) {
-  pos = scratch_home(key, kp.smask);
+// Find-only lookup (0 = not registered in this batch).
+__device__ __forceinline__ uint32_t scratch_find(const KParams& kp, uint64_t key) {
+  const unsigned long long kx = key ^ kp.salt;
+  uint64_t pos = scratch_home(key, kp.smask);
   for (uint64_t probes = 0; probes <= kp.smask; ++probes) {
-    unsigned long long k = *(volatile unsigned long long*)&kp.sl[pos].key;
-    if (k == key) return true;
-    if (k == 0) return false;
+    const ulonglong2 e = ldw128(&kp.stab[pos]);
+    if ((uint32_t)(e.y >> 32) != kp.epoch) return 0;
+    if (e.x == kx) return (uint32_t)e.y;
     pos = (pos + 1) & kp.smask;
   }
-  return false;
-}
-
-// Warp-aggregated append of newly created slots to the created list (for k_cleanup).
-__device__ __forceinline__ void append_created(const KParams& kp, bool created, uint64_t pos,
-                                               int lane, uint32_t seg) {
-  const uint32_t m = __ballot_sync(0xffffffffu, created);
-  if (!m) return;
-  uint32_t base = 0;
-  if (lane == 0) base = atomicAdd(&kp.seg_cnt[seg], (uint32_t)__popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (created) {
-    const uint32_t idx = base + __popc(m & ((1u << lane) - 1u));
-    if (idx < kp.seg_cap) kp.seg_list[(uint64_t)seg * kp.seg_cap + idx] = (uint32_t)pos;
-    else set_err(kp.st, ERR_SCRATCH);
-  }
-}
-
-// Is a staged value (tag << 32 | seq') visible to request seq' = seqp, reading round tag `tagR`?
-__device__ __forceinline__ bool staged_visible(unsigned long long v, uint32_t seqp, uint32_t tagR,
-                                               uint32_t tagS) {
-  const uint32_t tg = (uint32_t)(v >> 32);
-  return tg == tagS || (tg == tagR && (uint32_t)v < seqp);
+  return 0;
 }
 
 // ---------------------------------------------------------------------------------------------
 // K_A (round 0): hash + chained-prefix scan + registration.  One warp per request; lane = block
-// within a 32-block group.  Forward-exponent chain:
+// within a 32-block group; the next group's tokens are in flight while this group registers.
+// Forward-exponent chain:
 //   S[b] = sum_{t<=b} M^(t-1) * (h_t + sigma)   — a prefix SUM: warp shfl scan + scalar carry.
 // ---------------------------------------------------------------------------------------------
+template <int POLICY, int SH>
+__device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uint64_t j, int lane,
+                                                          const uint32_t* base, uint32_t n,
+                                                          uint64_t blk0, uint32_t u,
+                                                          uint32_t seg) {
+  const uint64_t sig = (POLICY == SOLID_POLICY_USER_ISOLATION) ? sigma_of(kp.seed, u) : 0;
+  const unsigned long long guess =
+      ((unsigned long long)tag_of(kp.epoch, 0) << 32) | (unsigned long long)(j + 1);
+  uint64_t carry = 0;
+  uint32_t bad = 0;
+  BlockWords<SH> cur, nxt;
+  if ((uint32_t)lane < n) cur.load(base + (uint64_t)kBS * lane);
+  for (uint32_t g = 0; g < n; g += 32) {
+    const uint32_t i = g + lane;
+    const bool valid = i < n;
+    if (i + 32 < n) nxt.load(base + (uint64_t)kBS * (i + 32));       // prefetch next group
+    uint64_t term = 0;
+    if (valid) term = mulmod(addmod(cur.hash(kp, bad), sig), kp.mpow[i]);
+    const uint64_t S = addmod(warp_scan_addmod(term, lane), carry);
+    carry = __shfl_sync(0xffffffffu, S, 31);
+    bool created = false;
+    const uint32_t id = scratch_register(kp, valid, key_of(S), seg, lane, created);
+    if (valid && id) {
+      kp.id_of_block[blk0 + i] = id;
+      // APC first-occurrence guess (P0, tag 0); the creator needs no read-before-atomic
+      if (created) atomicMin(&kp.hot[id].ins[0], guess);
+      else atomic_min_u64(&kp.hot[id].ins[0], guess);
+    }
+    cur = nxt;
+  }
+  return bad;
+}
+
 template <int POLICY>
 __global__ void __launch_bounds__(256) k_hash_register(KParams kp) {
   const int lane = threadIdx.x & 31;
@@ -301,50 +371,29 @@ __global__ void __launch_bounds__(256) k_hash_register(KParams kp) {
     return;
   }
   const uint32_t* base = kp.tokens + o0;
-  const int sh = (int)(((uintptr_t)base >> 2) & 3);
-  const uint64_t sig = (POLICY == SOLID_POLICY_USER_ISOLATION) ? sigma_of(kp.seed, u) : 0;
-  const unsigned long long guess =
-      ((unsigned long long)tag_of(kp.epoch, 0) << 32) | (unsigned long long)(j + 1);
-  uint64_t carry = 0;
-  uint32_t bad = 0;
-  for (uint32_t g = 0; g < n; g += 32) {
-    const uint32_t i = g + lane;
-    const bool valid = i < n;
-    uint64_t term = 0;
-    if (valid) {
-      const uint64_t h = hash_block(base + (uint64_t)kBS * i, sh, kp, bad);
-      term = mulmod(addmod(h, sig), kp.mpow[i]);
-    }
-    uint64_t S = addmod(warp_scan_addmod(term, lane), carry);
-    carry = __shfl_sync(0xffffffffu, S, 31);
-    bool created = false;
-    uint64_t pos = 0;
-    if (valid) {
-      pos = scratch_register(kp, key_of(S), created);
-      if (pos != ~0ull) {
-        kp.slot_of_block[blk0 + i] = (uint32_t)pos;
-        atomic_min_u64(&kp.sl[pos].st[0], guess);     // APC first-occurrence guess (P0, tag 0)
-      }
-    }
-    append_created(kp, created, pos, lane, seg);
+  uint32_t bad;
+  switch (((uintptr_t)base >> 2) & 3) {
+    case 0: bad = hash_register_request<POLICY, 0>(kp, j, lane, base, n, blk0, u, seg); break;
+    case 1: bad = hash_register_request<POLICY, 1>(kp, j, lane, base, n, blk0, u, seg); break;
+    case 2: bad = hash_register_request<POLICY, 2>(kp, j, lane, base, n, blk0, u, seg); break;
+    default: bad = hash_register_request<POLICY, 3>(kp, j, lane, base, n, blk0, u, seg); break;
   }
   if (__any_sync(0xffffffffu, bad != 0) && lane == 0) set_err(kp.st, ERR_TOKEN);
 }
 
 // ---------------------------------------------------------------------------------------------
 // K_B: one resolver round t (t >= 1) — the per-request Detector of P:454-459 evaluated against
-// "the state as of this request" reconstructed from round t-1's staged values.
+// "the state as of this request", reconstructed from round t-1's staged values.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t owner_from(const KParams& kp, const Slot* s,
+__device__ __forceinline__ uint32_t owner_from(const KParams& kp, uint32_t id,
                                                unsigned long long ins, uint32_t tagS) {
-  if ((uint32_t)(ins >> 32) == tagS) return s->snap_owner;
+  if ((uint32_t)(ins >> 32) == tagS) return kp.cold[id].snap_owner;
   return kp.users[(uint32_t)ins - 1u];
 }
 
 __device__ __forceinline__ uint64_t iso_key(const KParams& kp, uint64_t blk, uint32_t i,
                                             uint64_t sig, uint64_t gf) {
-  const uint32_t s = kp.slot_of_block[blk];
-  const uint64_t S = chain_of(kp.sl[s].key);
+  const uint64_t S = chain_of(kp.cold[kp.id_of_block[blk]].key);
   const uint64_t d = submod(kp.gtab[i + 1], gf);   // G[b] - G[f], b = i + 1
   return key_of(addmod(S, mulmod(sig, d)));
 }
@@ -369,6 +418,8 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
   const uint32_t tagR = tag_of(kp.epoch, t - 1), tagW = tag_of(kp.epoch, t),
                  tagS = tag_of(kp.epoch, kSubSnap);
   const bool enf = (POLICY == SOLID_POLICY_SOLIDARITY) && (kp.enforce ? kp.enforce[j] != 0 : true);
+  const uint4 prev =
+      (POLICY == SOLID_POLICY_SOLIDARITY && t >= 2) ? kp.dec[j] : make_uint4(0, 0, 0, 0);
 
   // ---- a5: first miss k (warp ballot) and barrier scan f over the Shared chain ----
   uint32_t k = n;
@@ -377,16 +428,15 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
   for (uint32_t g = 0; g <= n; g += 32) {
     const uint32_t i = g + lane;
     const bool valid = i < n;
-    uint32_t s = 0;
-    unsigned long long ins = 0, flg = 0;
+    uint32_t id = 0;
+    unsigned long long ins = 0;
     bool vis = false, fl = false;
     if (valid) {
-      s = kp.slot_of_block[blk0 + i];
-      const ulonglong2 v = ld_v2u64(&kp.sl[s].st[2 * R]);
-      ins = v.x;
-      flg = v.y;
+      id = kp.id_of_block[blk0 + i];
+      ins = ldw64(&kp.hot[id].ins[R]);
       vis = staged_visible(ins, seqp, tagR, tagS);
-      fl = staged_visible(flg, seqp, tagR, tagS);
+      if (POLICY == SOLID_POLICY_SOLIDARITY)
+        fl = staged_visible(ldw64(&kp.hot[id].flg[R]), seqp, tagR, tagS);
     }
     const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
     const int L = inv ? __ffs(inv) - 1 : 32;         // first invisible lane in this group
@@ -398,7 +448,7 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
       if (lane == 0) pf = carry_flag;
       bool cond = false;
       if (pf && lane <= L && !(g == 0 && lane == 0)) {
-        const bool pass = vis && owner_from(kp, &kp.sl[s], ins, tagS) == u;
+        const bool pass = vis && owner_from(kp, id, ins, tagS) == u;
         cond = !pass;
       }
       const uint32_t cm = __ballot_sync(0xffffffffu, cond);
@@ -414,29 +464,52 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
 
   // ---- selective isolation: continue in Iso(u) rooted at S[f] (R3) ----
   uint32_t r = k, flagd = 0;
-  uint64_t sig = 0, gf = 0;
   if (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) {
-    sig = sigma_of(kp.seed, u);
-    gf = kp.gtab[f];
     uint32_t m = n - (uint32_t)f;
-    for (uint32_t g = (uint32_t)f; g < n; g += 32) {
-      const uint32_t i = g + lane;
-      bool vis = false;
-      if (i < n) {
-        const uint64_t key = iso_key(kp, blk0 + i, i, sig, gf);
-        uint64_t pos;
-        if (scratch_find(kp, key, pos))
-          vis = staged_visible(kp.sl[pos].st[2 * R], seqp, tagR, tagS);
-        if (!vis) {
-          uint32_t ow, sr;
-          uint64_t ip;
-          vis = index_find(kp, key, ow, sr, ip);
+    if (t >= 2 && (int32_t)prev.y == f) {
+      // same divert depth as last round: the isolated keys of blocks f..n-1 are registered and
+      // their ids cached in iso_id[] (created in an earlier round, so the staged state already
+      // carries their index snapshot)
+      for (uint32_t g = (uint32_t)f; g < n; g += 32) {
+        const uint32_t i = g + lane;
+        bool vis = false;
+        if (i < n)
+          vis = staged_visible(ldw64(&kp.hot[kp.iso_id[blk0 + i]].ins[R]), seqp, tagR, tagS);
+        const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
+        if (inv) {
+          m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
+          break;
         }
       }
-      const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
-      if (inv) {
-        m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
-        break;
+    } else {
+      // new divert depth: derive I_f[b] = S[b] + sigma_u (G[b] - G[f]) for b > f, register every
+      // key (find-or-insert) and cache its id; visibility = staged (earlier batch requests) or
+      // present in the index snapshot
+      const uint64_t sig = sigma_of(kp.seed, u);
+      const uint64_t gf = kp.gtab[f];
+      bool found = false;
+      for (uint32_t g = (uint32_t)f; g < n; g += 32) {
+        const uint32_t i = g + lane;
+        const bool valid = i < n;
+        uint64_t key = 0;
+        if (valid) key = iso_key(kp, blk0 + i, i, sig, gf);
+        bool created;
+        const uint32_t id = scratch_register(kp, valid, key, seg, lane, created);
+        bool vis = false;
+        if (valid) {
+          kp.iso_id[blk0 + i] = id;
+          vis = staged_visible(ldw64(&kp.hot[id].ins[R]), seqp, tagR, tagS);
+          if (!vis) {
+            uint32_t ow, sr;
+            uint64_t ip;
+            vis = index_find(kp, key, ow, sr, ip);
+          }
+        }
+        const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
+        if (inv && !found) {
+          m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
+          found = true;
+        }
       }
     }
     r = (uint32_t)f + m;
@@ -444,12 +517,12 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
     // flag rule (R2): e_r = K[k] gets flagged iff owner != u and unflagged; applies with
     // isolation on or off (R11)
     if (lane == 0) {
-      const uint32_t s = kp.slot_of_block[blk0 + k - 1];
-      const ulonglong2 v = ld_v2u64(&kp.sl[s].st[2 * R]);
-      const bool flagged = staged_visible(v.y, seqp, tagR, tagS);
-      if (!flagged && owner_from(kp, &kp.sl[s], v.x, tagS) != u) {
+      const uint32_t id = kp.id_of_block[blk0 + k - 1];
+      const unsigned long long ins = ldw64(&kp.hot[id].ins[R]);
+      const bool flagged = staged_visible(ldw64(&kp.hot[id].flg[R]), seqp, tagR, tagS);
+      if (!flagged && owner_from(kp, id, ins, tagS) != u) {
         flagd = k;
-        atomic_min_u64(&kp.sl[s].st[2 * W + 1],
+        atomic_min_u64(&kp.hot[id].flg[W],
                        ((unsigned long long)tagW << 32) | (unsigned long long)seqp);
       }
     }
@@ -459,20 +532,8 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
   // ---- staged inserts (seq-min scatter); APC / USER_ISOLATION are exact from round 0 ----
   if (POLICY == SOLID_POLICY_SOLIDARITY) {
     const unsigned long long mine = ((unsigned long long)tagW << 32) | (unsigned long long)seqp;
-    for (uint32_t g = r; g < n; g += 32) {
-      const uint32_t i = g + lane;
-      bool created = false;
-      uint64_t pos = 0;
-      if (i < n) {
-        if (f >= 1) {
-          pos = scratch_register(kp, iso_key(kp, blk0 + i, i, sig, gf), created);
-        } else {
-          pos = kp.slot_of_block[blk0 + i];
-        }
-        if (pos != ~0ull) atomic_min_u64(&kp.sl[pos].st[2 * W], mine);
-      }
-      append_created(kp, created, pos, lane, seg);
-    }
+    const uint32_t* ids = (f >= 1) ? kp.iso_id : kp.id_of_block;
+    for (uint32_t i = r + lane; i < n; i += 32) atomic_min_u64(&kp.hot[ids[blk0 + i]].ins[W], mine);
   }
 
   if (lane == 0) {
@@ -480,9 +541,8 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
     if (POLICY == SOLID_POLICY_SOLIDARITY) {
       if (t == 1) {
         kp.st->changed[1] = 1;
-      } else {
-        const uint4 o = kp.dec[j];
-        if (o.x != d.x || o.y != d.y || o.z != d.z || o.w != d.w) kp.st->changed[t] = 1;
+      } else if (prev.x != d.x || prev.y != d.y || prev.z != d.z || prev.w != d.w) {
+        kp.st->changed[t] = 1;
       }
     }
     kp.dec[j] = d;
@@ -501,8 +561,9 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
 
 // ---------------------------------------------------------------------------------------------
 // K_C: commit.  The first inserter of each key (seq-min in the final state) claims an index slot
-// with one 128-bit CAS; the first flagger of a snapshot entry writes its sharer (a6).
-// mode 0 counts new entries (capacity check before any mutation), mode 1 commits.
+// with one 128-bit CAS {key, owner, sharer}; the first flagger of a snapshot entry writes its
+// sharer (a6).  mode 1 commits (optimistically) and counts; mode 2 rolls the batch back exactly:
+// every claimed slot was EMPTY before, so emptying it again restores the previous probe chains.
 // ---------------------------------------------------------------------------------------------
 template <int POLICY>
 __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mode) {
@@ -520,29 +581,17 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mod
     const uint4 d = kp.dec[j];
     const uint32_t r = d.z, flagd = d.w;
     const int32_t f = (int32_t)d.y;
-    uint64_t sig = 0, gf = 0;
-    if (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) {
-      sig = sigma_of(kp.seed, u);
-      gf = kp.gtab[f];
-    }
-    for (uint32_t g = r; g < n; g += 32) {
-      const uint32_t i = g + lane;
-      if (i >= n) break;
-      uint64_t pos;
-      uint64_t key;
-      if (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) {
-        key = iso_key(kp, blk0 + i, i, sig, gf);
-        if (!scratch_find(kp, key, pos)) continue;
-      } else {
-        pos = kp.slot_of_block[blk0 + i];
-        key = kp.sl[pos].key;
-      }
-      const Slot* s = kp.sl + pos;
-      const unsigned long long ins = s->st[2 * W];
-      if ((uint32_t)(ins >> 32) != tag || (uint32_t)ins != seqp) continue;   // not first inserter
+    const uint32_t* ids =
+        (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) ? kp.iso_id : kp.id_of_block;
+    for (uint32_t i = r + lane; i < n; i += 32) {
+      const uint32_t id = ids[blk0 + i];
+      const unsigned long long iv = ldw64(&kp.hot[id].ins[W]);
+      if ((uint32_t)(iv >> 32) != tag || (uint32_t)iv != seqp) continue;   // not first inserter
       ++cnt;
+      Cold* c = kp.cold + id;
+      const uint64_t key = c->key;
       if (mode == 1) {
-        const unsigned long long fv = s->st[2 * W + 1];
+        const unsigned long long fv = ldw64(&kp.hot[id].flg[W]);
         const uint32_t sharer =
             ((uint32_t)(fv >> 32) == tag) ? kp.users[(uint32_t)fv - 1u] : kNone;
         const ulonglong2 val = make_ulonglong2(key, (unsigned long long)u |
@@ -553,20 +602,20 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mod
           if (old.x == 0 || old.x == key) break;
           p = (p + 1) & kp.tmask;
         }
+        c->psl = (uint32_t)p;
+      } else {
+        kp.tab[c->psl] = make_ulonglong2(0ull, 0ull);
       }
     }
     if (POLICY == SOLID_POLICY_SOLIDARITY && flagd > 0 && lane == 0) {
-      const uint32_t sp = kp.slot_of_block[blk0 + flagd - 1];
-      const Slot* s = kp.sl + sp;
+      const uint32_t id = kp.id_of_block[blk0 + flagd - 1];
+      const unsigned long long iv = ldw64(&kp.hot[id].ins[W]), fv = ldw64(&kp.hot[id].flg[W]);
       const uint32_t tagS = tag_of(kp.epoch, kSubSnap);
-      const unsigned long long fv = s->st[2 * W + 1];
-      if ((uint32_t)(s->st[2 * W] >> 32) == tagS && (uint32_t)(fv >> 32) == tag &&
-          (uint32_t)fv == seqp) {
+      if ((uint32_t)(iv >> 32) == tagS && (uint32_t)(fv >> 32) == tag && (uint32_t)fv == seqp) {
         ++fcnt;
-        if (mode == 1) {
-          uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[s->psl].y) + 1;
-          atomicCAS(sharer_word, kNone, u);
-        }
+        uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
+        if (mode == 1) atomicCAS(sharer_word, kNone, u);
+        else atomicCAS(sharer_word, u, kNone);
       }
     }
   }
@@ -575,7 +624,7 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mod
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     fcnt += __shfl_xor_sync(0xffffffffu, fcnt, o);
   }
-  if (lane == 0 && mode == 0 && (cnt | fcnt)) {
+  if (lane == 0 && mode == 1 && (cnt | fcnt)) {
     atomicAdd(&kp.st->new_entries, (unsigned long long)cnt);
     atomicAdd(&kp.st->new_flags, (unsigned long long)fcnt);
   }
@@ -602,27 +651,10 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
   }
 }
 
-// Clear the scratch keys registered by this batch.
-__global__ void __launch_bounds__(256) k_cleanup(Slot* sl, const uint32_t* seg_cnt,
-                                                 const uint32_t* seg_list, uint32_t seg_cap) {
-  const uint32_t seg = blockIdx.y;
-  const uint32_t c = min(seg_cnt[seg], seg_cap);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
-    sl[seg_list[(uint64_t)seg * seg_cap + i]].key = 0ull;
-}
-
-__global__ void k_init_slots(Slot* sl, uint64_t n) {
+__global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long v) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    Slot s;
-    s.key = 0;
-    s.snap_owner = kNone;
-    s.snap_sharer = kNone;
-    s.psl = kNone;
-    s.pad[0] = s.pad[1] = s.pad[2] = 0;
-    s.st[0] = s.st[1] = s.st[2] = s.st[3] = ~0ull;
-    sl[i] = s;
-  }
+       i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = v;
 }
 
 }  // namespace solid
@@ -644,14 +676,17 @@ struct solid_ctx {
   uint64_t live = 0;
   ulonglong2* tab_ckpt = nullptr;
   uint64_t live_ckpt = 0;
-  // scratch
-  Slot* sl = nullptr;
+  // batch scratch
+  ulonglong2* stab = nullptr;
   uint64_t scap = 0;
-  uint32_t* slot_of_block = nullptr;
+  Hot* hot = nullptr;
+  Cold* cold = nullptr;
+  uint64_t idcap = 0;
+  uint32_t* id_of_block = nullptr;
+  uint32_t* iso_id = nullptr;
   uint64_t slot_cap = 0;
   uint4* dec = nullptr;
   uint32_t* seg_cnt = nullptr;
-  uint32_t* seg_list = nullptr;
   uint32_t seg_cap = 0;
   DevStatus* st = nullptr;
   DevStatus* st_host = nullptr;   // pinned mirror
@@ -708,11 +743,13 @@ extern "C" const char* solid_last_error(const solid_ctx* ctx) {
 static void free_all(solid_ctx* c) {
   cudaFree(c->tab);
   cudaFree(c->tab_ckpt);
-  cudaFree(c->sl);
-  cudaFree(c->slot_of_block);
+  cudaFree(c->stab);
+  cudaFree(c->hot);
+  cudaFree(c->cold);
+  cudaFree(c->id_of_block);
+  cudaFree(c->iso_id);
   cudaFree(c->dec);
   cudaFree(c->seg_cnt);
-  cudaFree(c->seg_list);
   cudaFree(c->st);
   cudaFree(c->mpow);
   cudaFree(c->gtab);
@@ -724,6 +761,17 @@ static void free_all(solid_ctx* c) {
   if (c->st_host) cudaFreeHost(c->st_host);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+}
+
+// (Re)initialise the batch scratch: key table stale, staged states at +inf.
+static solid_status init_scratch(solid_ctx* ctx, cudaStream_t s) {
+  CK(cudaMemsetAsync(ctx->stab, 0, ctx->scap * sizeof(ulonglong2), s));
+  k_fill_u64<<<4096, 256, 0, s>>>(reinterpret_cast<unsigned long long*>(ctx->hot),
+                                  ctx->idcap * (sizeof(Hot) / 8), ~0ull);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t), s));
+  ctx->epoch = 0;
+  return SOLID_OK;
 }
 
 extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
@@ -743,20 +791,26 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   CK(cudaSetDevice(ctx->dev));
   ctx->tcap = next_pow2(std::max<uint64_t>(2 * cfg->capacity_blocks, 1024));
   ctx->slot_cap = cfg->max_batch_tokens / kBS + 1;
-  ctx->scap = next_pow2(std::max<uint64_t>(4 * ctx->slot_cap, 4096));
-  if (ctx->tcap > (1ull << 32) || ctx->scap > (1ull << 32)) {   // slot indices are 32-bit
+  // distinct keys per batch <= Shared keys + isolated keys of every divert depth tried; ids are
+  // allocated from kNSeg segments chosen by request, each with 2x headroom over an even share
+  ctx->idcap = std::max<uint64_t>(2 * ctx->slot_cap, 1u << 16);
+  ctx->seg_cap = (uint32_t)std::min<uint64_t>(2 * ctx->idcap / kNSeg + 1024, 0x7FFFFFFFull);
+  ctx->idcap = (uint64_t)kNSeg * ctx->seg_cap + 1;
+  ctx->scap = next_pow2(2 * ctx->idcap);
+  if (ctx->tcap > (1ull << 32) || ctx->idcap > (1ull << 32)) {   // 32-bit slot / id indices
     delete ctx;
     return SOLID_ERR_INVALID;
   }
-  ctx->seg_cap = (uint32_t)std::min<uint64_t>(2 * ctx->scap / kNSeg + 1024, 0xFFFFFFF0ull);
   const uint64_t mb = cfg->max_blocks;
   auto alloc = [&](void** p, size_t bytes) -> bool { return cudaMalloc(p, bytes) == cudaSuccess; };
   bool ok = alloc((void**)&ctx->tab, ctx->tcap * sizeof(ulonglong2)) &&
-            alloc((void**)&ctx->sl, ctx->scap * sizeof(Slot)) &&
-            alloc((void**)&ctx->slot_of_block, ctx->slot_cap * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->stab, ctx->scap * sizeof(ulonglong2)) &&
+            alloc((void**)&ctx->hot, ctx->idcap * sizeof(Hot)) &&
+            alloc((void**)&ctx->cold, ctx->idcap * sizeof(Cold)) &&
+            alloc((void**)&ctx->id_of_block, ctx->slot_cap * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->iso_id, ctx->slot_cap * sizeof(uint32_t)) &&
             alloc((void**)&ctx->dec, cfg->max_batch_requests * sizeof(uint4)) &&
             alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(uint32_t)) &&
-            alloc((void**)&ctx->seg_list, (uint64_t)kNSeg * ctx->seg_cap * sizeof(uint32_t)) &&
             alloc((void**)&ctx->st, sizeof(DevStatus)) &&
             alloc((void**)&ctx->mpow, mb * sizeof(unsigned long long)) &&
             alloc((void**)&ctx->gtab, (mb + 1) * sizeof(unsigned long long)) &&
@@ -787,9 +841,8 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   CK(cudaMemcpy(ctx->mpow, mp.data(), mb * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->gtab, g.data(), (mb + 1) * 8, cudaMemcpyHostToDevice));
   CK(cudaMemset(ctx->tab, 0, ctx->tcap * sizeof(ulonglong2)));
-  k_init_slots<<<4096, 256>>>(ctx->sl, ctx->scap);
-  CK(cudaGetLastError());
-  CK(cudaMemset(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t)));
+  solid_status rc = init_scratch(ctx, 0);
+  if (rc != SOLID_OK) return rc;
   CK(cudaMemset(ctx->st, 0, sizeof(DevStatus)));
   for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   CK(cudaDeviceSynchronize());
@@ -830,13 +883,6 @@ static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
   }
 }
 
-static solid_status cleanup_scratch(solid_ctx* ctx, cudaStream_t s) {
-  k_cleanup<<<dim3(8, kNSeg), 256, 0, s>>>(ctx->sl, ctx->seg_cnt, ctx->seg_list, ctx->seg_cap);
-  CK(cudaGetLastError());
-  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t), s));
-  return SOLID_OK;
-}
-
 extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b, solid_result* out,
                                            void* stream) {
   if (!ctx) return SOLID_ERR_INVALID;
@@ -850,11 +896,11 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(ctx->dev));
   ctx->stream = s;
-  if (++ctx->epoch > kMaxEpoch) {     // tag space exhausted: re-initialise the staged states
-    k_init_slots<<<4096, 256, 0, s>>>(ctx->sl, ctx->scap);
-    CK(cudaGetLastError());
-    ctx->epoch = 1;
+  if (ctx->epoch + 1 > kMaxEpoch) {     // tag space exhausted: re-initialise the scratch
+    solid_status rc = init_scratch(ctx, s);
+    if (rc != SOLID_OK) return rc;
   }
+  ++ctx->epoch;
   KParams& kp = ctx->kp;
   memcpy(kp.klo, ctx->klo, sizeof(kp.klo));
   memcpy(kp.khi, ctx->khi, sizeof(kp.khi));
@@ -868,22 +914,27 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   kp.n = b->n_requests;
   kp.max_blocks = ctx->cfg.max_blocks;
   kp.epoch = ctx->epoch;
-  kp.sl = ctx->sl;
+  kp.salt = splitmix64(0x5A17ull ^ ((unsigned long long)ctx->epoch << 20));
+  kp.stab = ctx->stab;
   kp.smask = ctx->scap - 1;
+  kp.hot = ctx->hot;
+  kp.cold = ctx->cold;
   kp.tab = ctx->tab;
   kp.tmask = ctx->tcap - 1;
-  kp.slot_of_block = ctx->slot_of_block;
+  kp.id_of_block = ctx->id_of_block;
+  kp.iso_id = ctx->iso_id;
   kp.slot_cap = ctx->slot_cap;
   kp.dec = ctx->dec;
   kp.out = out;
   kp.seg_cnt = ctx->seg_cnt;
-  kp.seg_list = ctx->seg_list;
   kp.seg_cap = ctx->seg_cap;
   kp.st = ctx->st;
   CK(cudaMemsetAsync(ctx->st, 0, sizeof(DevStatus), s));
+  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t), s));
   CK(cudaEventRecord(ctx->ev[0], s));
   const uint64_t n = b->n_requests;
   uint32_t rounds = 0;
+  ctx->launches = 0;
   if (n) {
     const unsigned grid = grid_for_warps(n);
     switch (ctx->cfg.policy) {
@@ -893,15 +944,15 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
       default: k_hash_register<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(kp); break;
     }
     CK(cudaGetLastError());
+    ctx->launches = 1;
   }
   CK(cudaEventRecord(ctx->ev[1], s));
-  ctx->launches = n ? 1 : 0;
   if (n && ctx->cfg.policy != SOLID_POLICY_SOLIDARITY) {
     CK(cudaEventRecord(ctx->ev[4], s));
     launch_eval(ctx, 1, s);      // exact in one pass: round-0 first occurrences are final
     CK(cudaEventRecord(ctx->ev[5], s));
-    ctx->launches += 1;
     CK(cudaGetLastError());
+    ctx->launches += 1;
     ctx->tf = 0;
     rounds = 1;
     CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
@@ -926,10 +977,8 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
           conv = q;
           break;
         }
-      if (!conv && t > kMaxRounds) {
-        cleanup_scratch(ctx, s);
+      if (!conv && t > kMaxRounds)
         return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
-      }
       chunk = std::min<uint32_t>(chunk * 2, 64);
     }
     ctx->tf = conv;
@@ -941,9 +990,6 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   CK(cudaEventRecord(ctx->ev[2], s));
   if (ctx->st_host->err) {
     const uint32_t e = ctx->st_host->err;
-    solid_status rc = cleanup_scratch(ctx, s);
-    if (rc != SOLID_OK) return rc;
-    CK(cudaStreamSynchronize(s));
     std::string m = "invalid batch:";
     if (e & ERR_OFFSETS) m += " offsets";
     if (e & ERR_TOKEN) m += " token>=2^20";
@@ -966,31 +1012,23 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   CK(cudaSetDevice(ctx->dev));
   const uint64_t n = ctx->kp.n;
   if (n) {
-    launch_commit(ctx, 0, s);
+    launch_commit(ctx, 1, s);      // optimistic commit + count; exact rollback on overflow
     CK(cudaGetLastError());
-    ctx->launches += 1;
-    CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const uint64_t add = ctx->st_host->new_entries;
-    if (ctx->live + add > ctx->cfg.capacity_blocks) {
-      solid_status rc = cleanup_scratch(ctx, s);
-      ctx->pending = false;
-      if (rc != SOLID_OK) return rc;
-      return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9)");
-    }
-    launch_commit(ctx, 1, s);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
     k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(ctx->kp.out, n, ctx->st);
     CK(cudaGetLastError());
+    ctx->launches += 2;
   }
   CK(cudaEventRecord(ctx->ev[3], s));
   CK(cudaMemcpyAsync(ctx->seg_host, ctx->seg_cnt, sizeof(ctx->seg_host), cudaMemcpyDeviceToHost, s));
-  solid_status rc = cleanup_scratch(ctx, s);
-  if (rc != SOLID_OK) return rc;
-  ctx->launches += 1;
   CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  ctx->pending = false;
+  if (n && ctx->live + ctx->st_host->new_entries > ctx->cfg.capacity_blocks) {
+    launch_commit(ctx, 2, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9)");
+  }
   const DevStatus& h = *ctx->st_host;
   solid_stats_t& S = ctx->stats;
   S.batches += 1;
@@ -1005,16 +1043,16 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   S.live_entries = ctx->live;
   S.last_rounds = ctx->rounds;
   uint64_t distinct = 0;
-  for (int q = 0; q < kNSeg; ++q) distinct += ctx->seg_host[q];
+  for (int q = 0; q < kNSeg; ++q) distinct += std::min<uint32_t>(ctx->seg_host[q], ctx->seg_cap);
   S.last_distinct_keys = (uint32_t)std::min<uint64_t>(distinct, 0xFFFFFFFFull);
   S.last_kernel_launches = ctx->launches;
   S.last_requests = n;
   S.last_blocks = h.sums[0];
   S.last_inserted = h.new_entries;
   S.last_flagged = h.sums[2];
-  S.algorithmic_bytes = 64ull * h.sums[0] + 37ull * n + 16ull * h.new_entries + 4ull * h.new_flags;
+  S.algorithmic_bytes = 64ull * h.sums[0] + 37ull * n + 16ull * distinct + 16ull * h.new_entries +
+                        4ull * h.new_flags;
   ctx->ev_valid = true;
-  ctx->pending = false;
   return SOLID_OK;
 }
 
@@ -1097,10 +1135,9 @@ extern "C" solid_status solid_reset(solid_ctx* ctx) {
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaMemset(ctx->tab, 0, ctx->tcap * sizeof(ulonglong2)));
-  if (ctx->pending || ctx->poisoned) {
-    k_init_slots<<<4096, 256>>>(ctx->sl, ctx->scap);
-    CK(cudaGetLastError());
-    CK(cudaMemset(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t)));
+  if (ctx->poisoned) {
+    solid_status rc = init_scratch(ctx, 0);
+    if (rc != SOLID_OK) return rc;
   }
   CK(cudaDeviceSynchronize());
   ctx->live = 0;

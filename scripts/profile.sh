@@ -1,0 +1,13 @@
+# ncu launch list + full captures of the top kernels (one GPU; never multi-rank)
+set -x
+OUT=${OUT:-gpurun_out}
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --profile --steps 1 --warmup 1 --no-cpu > $OUT/launches_bench.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_hash_register -s 1 -c 1 \
+    -o $OUT/prof_hash -f python bench.py --profile --steps 1 --warmup 1 --no-cpu > $OUT/prof_hash.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_eval -s 4 -c 4 \
+    -o $OUT/prof_eval -f python bench.py --profile --steps 1 --warmup 1 --no-cpu > $OUT/prof_eval.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_commit -s 2 -c 2 \
+    -o $OUT/prof_commit -f python bench.py --profile --steps 1 --warmup 1 --no-cpu > $OUT/prof_commit.log 2>&1
+ls -la $OUT
