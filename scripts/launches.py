@@ -16,7 +16,7 @@ for r in rows[hi + 1:]:
 tot = 0.0
 for (i, name), m in per.items():
     t = m.get("gpu__time_duration.sum", ("0", ""))
-    tv = float(t[0].replace(",", "")) * (1e-3 if t[1] == "nsecond" else 1.0)
+    tv = float(t[0].replace(",", "")) * {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(t[1], 1.0)
     tot += tv
     extra = "  ".join(f"{k.split('__')[1].split('.')[0]}={v[0]} {v[1]}" for k, v in m.items()
                       if k != "gpu__time_duration.sum")
