@@ -206,7 +206,7 @@ __device__ __forceinline__ uint64_t scratch_home(uint64_t key, uint64_t mask) {
 
 // The creator of an id records the key and its index snapshot, and seeds both ping-pong states
 // with it (the snapshot tag is the smallest tag of the batch, so it is never displaced).
-__device__ void init_id(const KParams& kp, uint32_t id, uint64_t key) {
+__device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key) {
   uint32_t owner = kNone, sharer = kNone;
   uint64_t ipos = 0;
   const bool present = index_find(kp, key, owner, sharer, ipos);
@@ -227,13 +227,15 @@ __device__ void init_id(const KParams& kp, uint32_t id, uint64_t key) {
       atomicMin(&h->flg[1], v);
     }
   }
+  return present;
 }
 
 // Warp-cooperative find-or-insert of one key per active lane.  Returns the key's id (0 only on
 // scratch overflow); `created` is set for the lane whose CAS published the key.  New ids are
 // allocated with one atomic per warp and probe step (segment `seg`).
 __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool active, uint64_t key,
-                                                     uint32_t seg, int lane, bool& created) {
+                                                     uint32_t seg, int lane, bool& created,
+                                                     bool* snap_present = nullptr) {
   const unsigned long long kx = key ^ kp.salt;
   const uint32_t E = kp.epoch;
   uint64_t pos = scratch_home(key, kp.smask);
@@ -277,7 +279,8 @@ __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool act
             id = mine;
             created = true;
             done = true;
-            init_id(kp, id, key);
+            const bool pr = init_id(kp, id, key);
+            if (snap_present) *snap_present = pr;
           } else {
             e = old;                                // authoritative current value: re-examine
             have_e = true;                          // without trusting a possibly stale L1 line
@@ -422,42 +425,63 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
       (POLICY == SOLID_POLICY_SOLIDARITY && t >= 2) ? kp.dec[j] : make_uint4(0, 0, 0, 0);
 
   // ---- a5: first miss k (warp ballot) and barrier scan f over the Shared chain ----
+  // Blocks are walked 128 at a time: the ids and staged states of 4 groups of 32 are loaded
+  // together (two dependent memory latencies per 128 blocks), then evaluated group by group.
   uint32_t k = n;
   int32_t f = -1;
   bool carry_flag = false;    // flagged(index g-1) from the previous group
-  for (uint32_t g = 0; g <= n; g += 32) {
-    const uint32_t i = g + lane;
-    const bool valid = i < n;
-    uint32_t id = 0;
-    unsigned long long ins = 0;
-    bool vis = false, fl = false;
-    if (valid) {
-      id = kp.id_of_block[blk0 + i];
-      ins = ldw64(&kp.hot[id].ins[R]);
-      vis = staged_visible(ins, seqp, tagR, tagS);
-      if (POLICY == SOLID_POLICY_SOLIDARITY)
-        fl = staged_visible(ldw64(&kp.hot[id].flg[R]), seqp, tagR, tagS);
+  bool walked = false;
+  for (uint32_t base = 0; base <= n && !walked; base += 128) {
+    uint32_t idq[4];
+    unsigned long long insq[4], flgq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t i = base + 32 * q + lane;
+      idq[q] = i < n ? kp.id_of_block[blk0 + i] : 0u;
     }
-    const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
-    const int L = inv ? __ffs(inv) - 1 : 32;         // first invisible lane in this group
-    if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
-      // lane evaluates the barrier condition for index m = i - 1 (needs flagged(m) and the
-      // owner of the NEXT entry i): stop at m iff flagged(m) and not (i visible and
-      // owned by the requester).
-      bool pf = __shfl_up_sync(0xffffffffu, fl, 1);
-      if (lane == 0) pf = carry_flag;
-      bool cond = false;
-      if (pf && lane <= L && !(g == 0 && lane == 0)) {
-        const bool pass = vis && owner_from(kp, id, ins, tagS) == u;
-        cond = !pass;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t i = base + 32 * q + lane;
+      insq[q] = 0;
+      flgq[q] = 0;
+      if (i < n) {
+        insq[q] = ldw64(&kp.hot[idq[q]].ins[R]);
+        if (POLICY == SOLID_POLICY_SOLIDARITY) flgq[q] = ldw64(&kp.hot[idq[q]].flg[R]);
       }
-      const uint32_t cm = __ballot_sync(0xffffffffu, cond);
-      if (cm) f = (int32_t)(g + (uint32_t)(__ffs(cm) - 1));   // 1-based depth = m + 1 = i
-      carry_flag = __shfl_sync(0xffffffffu, fl, 31);
     }
-    if (L < 32) {
-      k = g + (uint32_t)L;
-      break;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t g = base + 32 * q;
+      if (g > n) break;
+      const uint32_t i = g + lane;
+      const bool valid = i < n;
+      const uint32_t id = idq[q];
+      const unsigned long long ins = insq[q];
+      const bool vis = valid && staged_visible(ins, seqp, tagR, tagS);
+      const bool fl = valid && POLICY == SOLID_POLICY_SOLIDARITY &&
+                      staged_visible(flgq[q], seqp, tagR, tagS);
+      const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
+      const int L = inv ? __ffs(inv) - 1 : 32;         // first invisible lane in this group
+      if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
+        // lane evaluates the barrier condition for index m = i - 1 (needs flagged(m) and the
+        // owner of the NEXT entry i): stop at m iff flagged(m) and not (i visible and
+        // owned by the requester).
+        bool pf = __shfl_up_sync(0xffffffffu, fl, 1);
+        if (lane == 0) pf = carry_flag;
+        bool cond = false;
+        if (pf && lane <= L && !(g == 0 && lane == 0)) {
+          const bool pass = vis && owner_from(kp, id, ins, tagS) == u;
+          cond = !pass;
+        }
+        const uint32_t cm = __ballot_sync(0xffffffffu, cond);
+        if (cm) f = (int32_t)(g + (uint32_t)(__ffs(cm) - 1));   // 1-based depth = m + 1 = i
+        carry_flag = __shfl_sync(0xffffffffu, fl, 31);
+      }
+      if (L < 32) {
+        k = g + (uint32_t)L;
+        walked = true;
+        break;
+      }
     }
   }
   if (POLICY == SOLID_POLICY_USER_ISOLATION) f = 0;
@@ -493,22 +517,35 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
         const bool valid = i < n;
         uint64_t key = 0;
         if (valid) key = iso_key(kp, blk0 + i, i, sig, gf);
-        bool created;
-        const uint32_t id = scratch_register(kp, valid, key, seg, lane, created);
-        bool vis = false;
+        bool created, snap = false;
+        const uint32_t id = scratch_register(kp, valid, key, seg, lane, created, &snap);
+        bool bvis = false;
         if (valid) {
           kp.iso_id[blk0 + i] = id;
-          vis = staged_visible(ldw64(&kp.hot[id].ins[R]), seqp, tagR, tagS);
-          if (!vis) {
-            uint32_t ow, sr;
-            uint64_t ip;
-            vis = index_find(kp, key, ow, sr, ip);
-          }
+          bvis = staged_visible(ldw64(&kp.hot[id].ins[R]), seqp, tagR, tagS);
         }
-        const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
-        if (inv && !found) {
-          m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
-          found = true;
+        // lanes not visible through the staged state may still be in the index snapshot; probe
+        // them in order, only until the first key that is absent (the walk stops there)
+        uint32_t cand = __ballot_sync(0xffffffffu, valid && !bvis);
+        while (!found && cand) {
+          const int L = __ffs(cand) - 1;
+          bool present = false;
+          if (lane == L) {
+            if (created) {
+              present = snap;
+            } else {
+              uint32_t ow, sr;
+              uint64_t ip;
+              present = index_find(kp, key, ow, sr, ip);
+            }
+          }
+          present = __shfl_sync(0xffffffffu, present, L);
+          if (present) {
+            cand &= cand - 1;
+          } else {
+            m = g + (uint32_t)L - (uint32_t)f;
+            found = true;
+          }
         }
       }
     }
@@ -560,41 +597,32 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// K_C: commit.  The first inserter of each key (seq-min in the final state) claims an index slot
-// with one 128-bit CAS {key, owner, sharer}; the first flagger of a snapshot entry writes its
-// sharer (a6).  mode 1 commits (optimistically) and counts; mode 2 rolls the batch back exactly:
+// K_C: commit, one thread per registered key (dense ids, coalesced).  In the converged state a
+// key carrying the final round's tag was inserted by the request in its low 32 bits (the
+// earliest one, "set exactly once"): it claims an index slot with one 128-bit CAS
+// {key, owner, sharer}.  A snapshot entry whose flag carries the final tag gets its sharer
+// written (a6).  mode 1 commits (optimistically) and counts; mode 2 rolls the batch back exactly:
 // every claimed slot was EMPTY before, so emptying it again restores the previous probe chains.
 // ---------------------------------------------------------------------------------------------
-template <int POLICY>
 __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mode) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  uint32_t cnt = 0, fcnt = 0;
-  if (j < kp.n) {
-    const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
-    const uint32_t n = (uint32_t)((o1 - o0) >> 4);
-    const uint64_t blk0 = o0 >> 4;
-    const uint32_t u = kp.users[j];
-    const uint32_t seqp = (uint32_t)(j + 1);
-    const int W = (int)(tf & 1);
-    const uint32_t tag = tag_of(kp.epoch, tf);
-    const uint4 d = kp.dec[j];
-    const uint32_t r = d.z, flagd = d.w;
-    const int32_t f = (int32_t)d.y;
-    const uint32_t* ids =
-        (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) ? kp.iso_id : kp.id_of_block;
-    for (uint32_t i = r + lane; i < n; i += 32) {
-      const uint32_t id = ids[blk0 + i];
-      const unsigned long long iv = ldw64(&kp.hot[id].ins[W]);
-      if ((uint32_t)(iv >> 32) != tag || (uint32_t)iv != seqp) continue;   // not first inserter
-      ++cnt;
+  const uint32_t seg = blockIdx.y;
+  const uint32_t cnt = min(kp.seg_cnt[seg], kp.seg_cap);
+  const int W = (int)(tf & 1);
+  const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
+  uint32_t c_new = 0, c_flag = 0;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * blockDim.x) {
+    const uint32_t id = seg * kp.seg_cap + x + 1;
+    const unsigned long long iv = ldw64(&kp.hot[id].ins[W]);
+    const unsigned long long fv = ldw64(&kp.hot[id].flg[W]);
+    const uint32_t itag = (uint32_t)(iv >> 32);
+    if (itag == tag) {
+      ++c_new;
       Cold* c = kp.cold + id;
-      const uint64_t key = c->key;
       if (mode == 1) {
-        const unsigned long long fv = ldw64(&kp.hot[id].flg[W]);
-        const uint32_t sharer =
-            ((uint32_t)(fv >> 32) == tag) ? kp.users[(uint32_t)fv - 1u] : kNone;
-        const ulonglong2 val = make_ulonglong2(key, (unsigned long long)u |
+        const uint64_t key = c->key;
+        const uint32_t owner = kp.users[(uint32_t)iv - 1u];
+        const uint32_t sharer = ((uint32_t)(fv >> 32) == tag) ? kp.users[(uint32_t)fv - 1u] : kNone;
+        const ulonglong2 val = make_ulonglong2(key, (unsigned long long)owner |
                                                         ((unsigned long long)sharer << 32));
         uint64_t p = key & kp.tmask;
         for (;;) {
@@ -606,27 +634,21 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mod
       } else {
         kp.tab[c->psl] = make_ulonglong2(0ull, 0ull);
       }
-    }
-    if (POLICY == SOLID_POLICY_SOLIDARITY && flagd > 0 && lane == 0) {
-      const uint32_t id = kp.id_of_block[blk0 + flagd - 1];
-      const unsigned long long iv = ldw64(&kp.hot[id].ins[W]), fv = ldw64(&kp.hot[id].flg[W]);
-      const uint32_t tagS = tag_of(kp.epoch, kSubSnap);
-      if ((uint32_t)(iv >> 32) == tagS && (uint32_t)(fv >> 32) == tag && (uint32_t)fv == seqp) {
-        ++fcnt;
-        uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
-        if (mode == 1) atomicCAS(sharer_word, kNone, u);
-        else atomicCAS(sharer_word, u, kNone);
-      }
+    } else if (itag == tagS && (uint32_t)(fv >> 32) == tag) {
+      ++c_flag;
+      const uint32_t who = kp.users[(uint32_t)fv - 1u];
+      uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
+      if (mode == 1) atomicCAS(sharer_word, kNone, who);
+      else atomicCAS(sharer_word, who, kNone);
     }
   }
-  // warp reduce the counts, one atomic per warp
   for (int o = 16; o; o >>= 1) {
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    fcnt += __shfl_xor_sync(0xffffffffu, fcnt, o);
+    c_new += __shfl_xor_sync(0xffffffffu, c_new, o);
+    c_flag += __shfl_xor_sync(0xffffffffu, c_flag, o);
   }
-  if (lane == 0 && mode == 1 && (cnt | fcnt)) {
-    atomicAdd(&kp.st->new_entries, (unsigned long long)cnt);
-    atomicAdd(&kp.st->new_flags, (unsigned long long)fcnt);
+  if ((threadIdx.x & 31) == 0 && mode == 1 && (c_new | c_flag)) {
+    atomicAdd(&kp.st->new_entries, (unsigned long long)c_new);
+    atomicAdd(&kp.st->new_flags, (unsigned long long)c_flag);
   }
 }
 
@@ -874,13 +896,7 @@ static void launch_eval(solid_ctx* c, uint32_t t, cudaStream_t s) {
 }
 
 static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
-  const unsigned grid = grid_for_warps(c->kp.n);
-  switch (c->cfg.policy) {
-    case SOLID_POLICY_APC: k_commit<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(c->kp, c->tf, mode); break;
-    case SOLID_POLICY_USER_ISOLATION:
-      k_commit<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(c->kp, c->tf, mode); break;
-    default: k_commit<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(c->kp, c->tf, mode); break;
-  }
+  k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, c->tf, mode);
 }
 
 extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b, solid_result* out,

@@ -1,0 +1,10 @@
+set -x
+OUT=${OUT:-gpurun_out}
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_commit -s 1 -c 1 \
+    -o $OUT/prof_commit -f python bench.py --profile --steps 1 --warmup 1 --no-cpu > $OUT/prof_commit.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_eval -s 4 -c 4 \
+    -o $OUT/prof_eval -f python bench.py --profile --steps 1 --warmup 1 --no-cpu > $OUT/prof_eval.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_hash_register -s 1 -c 1 \
+    -o $OUT/prof_hash -f python bench.py --profile --steps 1 --warmup 1 --no-cpu > $OUT/prof_hash.log 2>&1
+ls -la $OUT
