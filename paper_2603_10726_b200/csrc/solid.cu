@@ -141,11 +141,20 @@ __device__ __forceinline__ void atomic_min_u64(unsigned long long* a, unsigned l
   if (ldw64(a) > v) atomicMin(a, v);
 }
 
-// Is a staged value (tag << 32 | seq') visible to request seq' = seqp, reading round tag `tagR`?
-__device__ __forceinline__ bool staged_visible(unsigned long long v, uint32_t seqp, uint32_t tagR,
-                                               uint32_t tagS) {
-  const uint32_t tg = (uint32_t)(v >> 32);
-  return tg == tagS || (tg == tagR && (uint32_t)v < seqp);
+// Round-t view of a ping-pong pair {P0, P1} of one key: the earliest request (seq' >= 1, or 0 for
+// the index snapshot) visible to request seqp, reading round t-1's complete values (tagR in P[R])
+// and the round-t values already published in P[W] (Gauss-Seidel).  kNone if none is visible.
+// Mixing in partial round-t values never breaks exactness: a round whose decisions all equal the
+// previous round's certifies the sequential fixed point, and requests < t are final after round t.
+__device__ __forceinline__ uint32_t gs_first(ulonglong2 v, int R, uint32_t seqp, uint32_t tagR,
+                                             uint32_t tagW, uint32_t tagS) {
+  const unsigned long long a = R ? v.y : v.x, b = R ? v.x : v.y;
+  const uint32_t ta = (uint32_t)(a >> 32), tb = (uint32_t)(b >> 32);
+  if (ta == tagS || tb == tagS) return 0;
+  uint32_t s = kNone;
+  if (ta == tagR && (uint32_t)a < seqp) s = (uint32_t)a;
+  if (tb == tagW && (uint32_t)b < seqp) s = min(s, (uint32_t)b);
+  return s;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -388,10 +397,8 @@ __global__ void __launch_bounds__(256) k_hash_register(KParams kp) {
 // K_B: one resolver round t (t >= 1) — the per-request Detector of P:454-459 evaluated against
 // "the state as of this request", reconstructed from round t-1's staged values.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t owner_from(const KParams& kp, uint32_t id,
-                                               unsigned long long ins, uint32_t tagS) {
-  if ((uint32_t)(ins >> 32) == tagS) return kp.cold[id].snap_owner;
-  return kp.users[(uint32_t)ins - 1u];
+__device__ __forceinline__ uint32_t owner_from(const KParams& kp, uint32_t id, uint32_t first) {
+  return first == 0 ? kp.cold[id].snap_owner : kp.users[first - 1u];
 }
 
 __device__ __forceinline__ uint64_t iso_key(const KParams& kp, uint64_t blk, uint32_t i,
@@ -431,35 +438,35 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
   int32_t f = -1;
   bool carry_flag = false;    // flagged(index g-1) from the previous group
   bool walked = false;
-  for (uint32_t base = 0; base <= n && !walked; base += 128) {
-    uint32_t idq[4];
-    unsigned long long insq[4], flgq[4];
+  for (uint32_t base = 0; base <= n && !walked; base += 64) {
+    uint32_t idq[2];
+    ulonglong2 ivq[2], fvq[2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 2; ++q) {
       const uint32_t i = base + 32 * q + lane;
       idq[q] = i < n ? kp.id_of_block[blk0 + i] : 0u;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 2; ++q) {
       const uint32_t i = base + 32 * q + lane;
-      insq[q] = 0;
-      flgq[q] = 0;
+      ivq[q] = make_ulonglong2(~0ull, ~0ull);
+      fvq[q] = make_ulonglong2(~0ull, ~0ull);
       if (i < n) {
-        insq[q] = ldw64(&kp.hot[idq[q]].ins[R]);
-        if (POLICY == SOLID_POLICY_SOLIDARITY) flgq[q] = ldw64(&kp.hot[idq[q]].flg[R]);
+        ivq[q] = ldw128(&kp.hot[idq[q]].ins[0]);
+        if (POLICY == SOLID_POLICY_SOLIDARITY) fvq[q] = ldw128(&kp.hot[idq[q]].flg[0]);
       }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 2; ++q) {
       const uint32_t g = base + 32 * q;
       if (g > n) break;
       const uint32_t i = g + lane;
       const bool valid = i < n;
       const uint32_t id = idq[q];
-      const unsigned long long ins = insq[q];
-      const bool vis = valid && staged_visible(ins, seqp, tagR, tagS);
+      const uint32_t first = valid ? gs_first(ivq[q], R, seqp, tagR, tagW, tagS) : kNone;
+      const bool vis = first != kNone;
       const bool fl = valid && POLICY == SOLID_POLICY_SOLIDARITY &&
-                      staged_visible(flgq[q], seqp, tagR, tagS);
+                      gs_first(fvq[q], R, seqp, tagR, tagW, tagS) != kNone;
       const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
       const int L = inv ? __ffs(inv) - 1 : 32;         // first invisible lane in this group
       if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
@@ -470,7 +477,7 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
         if (lane == 0) pf = carry_flag;
         bool cond = false;
         if (pf && lane <= L && !(g == 0 && lane == 0)) {
-          const bool pass = vis && owner_from(kp, id, ins, tagS) == u;
+          const bool pass = vis && owner_from(kp, id, first) == u;
           cond = !pass;
         }
         const uint32_t cm = __ballot_sync(0xffffffffu, cond);
@@ -498,7 +505,8 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
         const uint32_t i = g + lane;
         bool vis = false;
         if (i < n)
-          vis = staged_visible(ldw64(&kp.hot[kp.iso_id[blk0 + i]].ins[R]), seqp, tagR, tagS);
+          vis = gs_first(ldw128(&kp.hot[kp.iso_id[blk0 + i]].ins[0]), R, seqp, tagR, tagW,
+                         tagS) != kNone;
         const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
         if (inv) {
           m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
@@ -522,7 +530,7 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
         bool bvis = false;
         if (valid) {
           kp.iso_id[blk0 + i] = id;
-          bvis = staged_visible(ldw64(&kp.hot[id].ins[R]), seqp, tagR, tagS);
+          bvis = gs_first(ldw128(&kp.hot[id].ins[0]), R, seqp, tagR, tagW, tagS) != kNone;
         }
         // lanes not visible through the staged state may still be in the index snapshot; probe
         // them in order, only until the first key that is absent (the walk stops there)
@@ -555,9 +563,10 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
     // isolation on or off (R11)
     if (lane == 0) {
       const uint32_t id = kp.id_of_block[blk0 + k - 1];
-      const unsigned long long ins = ldw64(&kp.hot[id].ins[R]);
-      const bool flagged = staged_visible(ldw64(&kp.hot[id].flg[R]), seqp, tagR, tagS);
-      if (!flagged && owner_from(kp, id, ins, tagS) != u) {
+      const uint32_t first = gs_first(ldw128(&kp.hot[id].ins[0]), R, seqp, tagR, tagW, tagS);
+      const bool flagged =
+          gs_first(ldw128(&kp.hot[id].flg[0]), R, seqp, tagR, tagW, tagS) != kNone;
+      if (!flagged && owner_from(kp, id, first) != u) {
         flagd = k;
         atomic_min_u64(&kp.hot[id].flg[W],
                        ((unsigned long long)tagW << 32) | (unsigned long long)seqp);
