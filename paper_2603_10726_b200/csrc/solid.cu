@@ -42,9 +42,8 @@ enum : uint32_t {
   ERR_OFFSETS = 1, ERR_TOKEN = 2, ERR_USER = 4, ERR_BLOCKS = 8, ERR_SCRATCH = 16, ERR_SLOTCAP = 32
 };
 
-struct __align__(32) Hot {            // staged state of one key (ping-pong by round parity)
-  unsigned long long ins[2];          // first inserter: tag << 32 | seq'
-  unsigned long long flg[2];          // first flagger:  tag << 32 | seq'
+struct __align__(32) Hot {            // staged state of one key, ping-pong by round parity P:
+  unsigned long long v[4];            // v[2P] first inserter, v[2P+1] first flagger (tag<<32|seq')
 };
 struct Cold {                         // the key and its index snapshot at batch start
   unsigned long long key;
@@ -146,15 +145,24 @@ __device__ __forceinline__ void atomic_min_u64(unsigned long long* a, unsigned l
 // and the round-t values already published in P[W] (Gauss-Seidel).  kNone if none is visible.
 // Mixing in partial round-t values never breaks exactness: a round whose decisions all equal the
 // previous round's certifies the sequential fixed point, and requests < t are final after round t.
-__device__ __forceinline__ uint32_t gs_first(ulonglong2 v, int R, uint32_t seqp, uint32_t tagR,
-                                             uint32_t tagW, uint32_t tagS) {
-  const unsigned long long a = R ? v.y : v.x, b = R ? v.x : v.y;
+__device__ __forceinline__ uint32_t gs_first(unsigned long long p0, unsigned long long p1, int R,
+                                             uint32_t seqp, uint32_t tagR, uint32_t tagW,
+                                             uint32_t tagS) {
+  const unsigned long long a = R ? p1 : p0, b = R ? p0 : p1;
   const uint32_t ta = (uint32_t)(a >> 32), tb = (uint32_t)(b >> 32);
   if (ta == tagS || tb == tagS) return 0;
   uint32_t s = kNone;
   if (ta == tagR && (uint32_t)a < seqp) s = (uint32_t)a;
   if (tb == tagW && (uint32_t)b < seqp) s = min(s, (uint32_t)b);
   return s;
+}
+
+// Jacobi view (round t-1's complete values only): seq' of the first request, 0 = snapshot, kNone.
+__device__ __forceinline__ uint32_t jacobi_first(unsigned long long v, uint32_t seqp,
+                                                 uint32_t tagR, uint32_t tagS) {
+  const uint32_t tg = (uint32_t)(v >> 32);
+  if (tg == tagS) return 0;
+  return (tg == tagR && (uint32_t)v < seqp) ? (uint32_t)v : kNone;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -229,11 +237,11 @@ __device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key) {
   if (present) {
     Hot* h = kp.hot + id;
     const unsigned long long v = (unsigned long long)tag_of(kp.epoch, kSubSnap) << 32;
-    atomicMin(&h->ins[0], v);
-    atomicMin(&h->ins[1], v);
+    atomicMin(&h->v[0], v);
+    atomicMin(&h->v[2], v);
     if (sharer != kNone) {
-      atomicMin(&h->flg[0], v);
-      atomicMin(&h->flg[1], v);
+      atomicMin(&h->v[1], v);
+      atomicMin(&h->v[3], v);
     }
   }
   return present;
@@ -350,8 +358,8 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
     if (valid && id) {
       kp.id_of_block[blk0 + i] = id;
       // APC first-occurrence guess (P0, tag 0); the creator needs no read-before-atomic
-      if (created) atomicMin(&kp.hot[id].ins[0], guess);
-      else atomic_min_u64(&kp.hot[id].ins[0], guess);
+      if (created) atomicMin(&kp.hot[id].v[0], guess);
+      else atomic_min_u64(&kp.hot[id].v[0], guess);
     }
     cur = nxt;
   }
@@ -408,6 +416,12 @@ __device__ __forceinline__ uint64_t iso_key(const KParams& kp, uint64_t blk, uin
   return key_of(addmod(S, mulmod(sig, d)));
 }
 
+__device__ __forceinline__ uint32_t iso_first(const KParams& kp, uint32_t id, int R, uint32_t seqp,
+                                              uint32_t tagR, uint32_t tagW, uint32_t tagS) {
+  const Hot* h = kp.hot + id;
+  return gs_first(ldw64(&h->v[0]), ldw64(&h->v[2]), R, seqp, tagR, tagW, tagS);
+}
+
 template <int POLICY>
 __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
   if (t >= 2 && kp.st->changed[t - 1] == 0) return;     // converged in an earlier round
@@ -416,57 +430,61 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
   if (j >= kp.n) return;
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
   const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
+  const uint32_t u = kp.users[j];
+  const bool enf = (POLICY == SOLID_POLICY_SOLIDARITY) && (kp.enforce ? kp.enforce[j] != 0 : true);
+  const uint4 prev =
+      (POLICY == SOLID_POLICY_SOLIDARITY && t >= 2) ? kp.dec[j] : make_uint4(0, ~0u, 0, 0);
   if (o1 < o0) return;
   const uint64_t nb = (o1 - o0) >> 4;
   if (nb > kp.max_blocks) return;
   const uint32_t n = (uint32_t)nb;
   const uint64_t blk0 = o0 >> 4;
   if (n && blk0 + n > kp.slot_cap) return;
-  const uint32_t u = kp.users[j];
   const uint32_t seqp = (uint32_t)(j + 1);
   const int R = (int)((t - 1) & 1), W = (int)(t & 1);
   const uint32_t tagR = tag_of(kp.epoch, t - 1), tagW = tag_of(kp.epoch, t),
                  tagS = tag_of(kp.epoch, kSubSnap);
-  const bool enf = (POLICY == SOLID_POLICY_SOLIDARITY) && (kp.enforce ? kp.enforce[j] != 0 : true);
-  const uint4 prev =
-      (POLICY == SOLID_POLICY_SOLIDARITY && t >= 2) ? kp.dec[j] : make_uint4(0, 0, 0, 0);
+  // speculation: last round's divert depth; its isolated ids are cached in iso_id[]
+  const int32_t fprev = (int32_t)prev.y;
+  uint32_t iso_pre_id = 0;
+  if (POLICY == SOLID_POLICY_SOLIDARITY && fprev >= 1 && (uint32_t)fprev + lane < n)
+    iso_pre_id = kp.iso_id[blk0 + (uint32_t)fprev + lane];
 
   // ---- a5: first miss k (warp ballot) and barrier scan f over the Shared chain ----
-  // Blocks are walked 128 at a time: the ids and staged states of 4 groups of 32 are loaded
-  // together (two dependent memory latencies per 128 blocks), then evaluated group by group.
+  // Blocks are walked 128 at a time: the ids and staged pairs P[R] = {first inserter, first
+  // flagger} of 4 groups of 32 are in flight together, then evaluated group by group.
   uint32_t k = n;
   int32_t f = -1;
   bool carry_flag = false;    // flagged(index g-1) from the previous group
   bool walked = false;
-  for (uint32_t base = 0; base <= n && !walked; base += 64) {
-    uint32_t idq[2];
-    ulonglong2 ivq[2], fvq[2];
+  uint32_t iso_pre_first = kNone;
+  for (uint32_t base = 0; base <= n && !walked; base += 128) {
+    uint32_t idq[4];
+    ulonglong2 pq[4];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < 4; ++q) {
       const uint32_t i = base + 32 * q + lane;
       idq[q] = i < n ? kp.id_of_block[blk0 + i] : 0u;
     }
+    if (POLICY == SOLID_POLICY_SOLIDARITY && base == 0 && fprev >= 1 && (uint32_t)fprev + lane < n)
+      iso_pre_first = iso_first(kp, iso_pre_id, R, seqp, tagR, tagW, tagS);
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < 4; ++q) {
       const uint32_t i = base + 32 * q + lane;
-      ivq[q] = make_ulonglong2(~0ull, ~0ull);
-      fvq[q] = make_ulonglong2(~0ull, ~0ull);
-      if (i < n) {
-        ivq[q] = ldw128(&kp.hot[idq[q]].ins[0]);
-        if (POLICY == SOLID_POLICY_SOLIDARITY) fvq[q] = ldw128(&kp.hot[idq[q]].flg[0]);
-      }
+      pq[q] = make_ulonglong2(~0ull, ~0ull);
+      if (i < n) pq[q] = ldw128(&kp.hot[idq[q]].v[2 * R]);
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < 4; ++q) {
       const uint32_t g = base + 32 * q;
       if (g > n) break;
       const uint32_t i = g + lane;
       const bool valid = i < n;
       const uint32_t id = idq[q];
-      const uint32_t first = valid ? gs_first(ivq[q], R, seqp, tagR, tagW, tagS) : kNone;
+      const uint32_t first = valid ? jacobi_first(pq[q].x, seqp, tagR, tagS) : kNone;
       const bool vis = first != kNone;
       const bool fl = valid && POLICY == SOLID_POLICY_SOLIDARITY &&
-                      gs_first(fvq[q], R, seqp, tagR, tagW, tagS) != kNone;
+                      jacobi_first(pq[q].y, seqp, tagR, tagS) != kNone;
       const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
       const int L = inv ? __ffs(inv) - 1 : 32;         // first invisible lane in this group
       if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
@@ -497,16 +515,15 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
   uint32_t r = k, flagd = 0;
   if (POLICY == SOLID_POLICY_SOLIDARITY && f >= 1) {
     uint32_t m = n - (uint32_t)f;
-    if (t >= 2 && (int32_t)prev.y == f) {
+    if (f == fprev) {
       // same divert depth as last round: the isolated keys of blocks f..n-1 are registered and
       // their ids cached in iso_id[] (created in an earlier round, so the staged state already
-      // carries their index snapshot)
+      // carries their index snapshot); the first group was prefetched above
       for (uint32_t g = (uint32_t)f; g < n; g += 32) {
         const uint32_t i = g + lane;
         bool vis = false;
-        if (i < n)
-          vis = gs_first(ldw128(&kp.hot[kp.iso_id[blk0 + i]].ins[0]), R, seqp, tagR, tagW,
-                         tagS) != kNone;
+        if (g == (uint32_t)f) vis = i < n && iso_pre_first != kNone;
+        else if (i < n) vis = iso_first(kp, kp.iso_id[blk0 + i], R, seqp, tagR, tagW, tagS) != kNone;
         const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
         if (inv) {
           m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
@@ -530,7 +547,7 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
         bool bvis = false;
         if (valid) {
           kp.iso_id[blk0 + i] = id;
-          bvis = gs_first(ldw128(&kp.hot[id].ins[0]), R, seqp, tagR, tagW, tagS) != kNone;
+          bvis = iso_first(kp, id, R, seqp, tagR, tagW, tagS) != kNone;
         }
         // lanes not visible through the staged state may still be in the index snapshot; probe
         // them in order, only until the first key that is absent (the walk stops there)
@@ -563,12 +580,13 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
     // isolation on or off (R11)
     if (lane == 0) {
       const uint32_t id = kp.id_of_block[blk0 + k - 1];
-      const uint32_t first = gs_first(ldw128(&kp.hot[id].ins[0]), R, seqp, tagR, tagW, tagS);
-      const bool flagged =
-          gs_first(ldw128(&kp.hot[id].flg[0]), R, seqp, tagR, tagW, tagS) != kNone;
+      const Hot* h = kp.hot + id;
+      const ulonglong2 p0 = ldw128(&h->v[0]), p1 = ldw128(&h->v[2]);
+      const uint32_t first = gs_first(p0.x, p1.x, R, seqp, tagR, tagW, tagS);
+      const bool flagged = gs_first(p0.y, p1.y, R, seqp, tagR, tagW, tagS) != kNone;
       if (!flagged && owner_from(kp, id, first) != u) {
         flagd = k;
-        atomic_min_u64(&kp.hot[id].flg[W],
+        atomic_min_u64(&kp.hot[id].v[2 * W + 1],
                        ((unsigned long long)tagW << 32) | (unsigned long long)seqp);
       }
     }
@@ -579,7 +597,7 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
   if (POLICY == SOLID_POLICY_SOLIDARITY) {
     const unsigned long long mine = ((unsigned long long)tagW << 32) | (unsigned long long)seqp;
     const uint32_t* ids = (f >= 1) ? kp.iso_id : kp.id_of_block;
-    for (uint32_t i = r + lane; i < n; i += 32) atomic_min_u64(&kp.hot[ids[blk0 + i]].ins[W], mine);
+    for (uint32_t i = r + lane; i < n; i += 32) atomic_min_u64(&kp.hot[ids[blk0 + i]].v[2 * W], mine);
   }
 
   if (lane == 0) {
@@ -621,8 +639,8 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mod
   uint32_t c_new = 0, c_flag = 0;
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * blockDim.x) {
     const uint32_t id = seg * kp.seg_cap + x + 1;
-    const unsigned long long iv = ldw64(&kp.hot[id].ins[W]);
-    const unsigned long long fv = ldw64(&kp.hot[id].flg[W]);
+    const ulonglong2 pw = ldw128(&kp.hot[id].v[2 * W]);
+    const unsigned long long iv = pw.x, fv = pw.y;
     const uint32_t itag = (uint32_t)(iv >> 32);
     if (itag == tag) {
       ++c_new;
