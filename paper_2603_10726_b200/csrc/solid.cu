@@ -424,16 +424,18 @@ __device__ __forceinline__ uint32_t iso_first(const KParams& kp, uint32_t id, in
 
 template <int POLICY>
 __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
-  if (t >= 2 && kp.st->changed[t - 1] == 0) return;     // converged in an earlier round
   const int lane = threadIdx.x & 31;
   const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= kp.n) return;
+  // all per-request loads are issued before the convergence test so their latencies overlap
+  const uint32_t more = (t >= 2) ? kp.st->changed[t - 1] : 1u;
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
   const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
   const uint32_t u = kp.users[j];
   const bool enf = (POLICY == SOLID_POLICY_SOLIDARITY) && (kp.enforce ? kp.enforce[j] != 0 : true);
   const uint4 prev =
       (POLICY == SOLID_POLICY_SOLIDARITY && t >= 2) ? kp.dec[j] : make_uint4(0, ~0u, 0, 0);
+  if (more == 0) return;                                 // converged in an earlier round
   if (o1 < o0) return;
   const uint64_t nb = (o1 - o0) >> 4;
   if (nb > kp.max_blocks) return;
@@ -490,17 +492,20 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
       if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
         // lane evaluates the barrier condition for index m = i - 1 (needs flagged(m) and the
         // owner of the NEXT entry i): stop at m iff flagged(m) and not (i visible and
-        // owned by the requester).
-        bool pf = __shfl_up_sync(0xffffffffu, fl, 1);
-        if (lane == 0) pf = carry_flag;
-        bool cond = false;
-        if (pf && lane <= L && !(g == 0 && lane == 0)) {
-          const bool pass = vis && owner_from(kp, id, first) == u;
-          cond = !pass;
+        // owned by the requester).  Groups without flagged entries skip it (the common case).
+        const uint32_t flm = __ballot_sync(0xffffffffu, fl);
+        if (flm || carry_flag) {
+          bool pf = __shfl_up_sync(0xffffffffu, fl, 1);
+          if (lane == 0) pf = carry_flag;
+          bool cond = false;
+          if (pf && lane <= L && !(g == 0 && lane == 0)) {
+            const bool pass = vis && owner_from(kp, id, first) == u;
+            cond = !pass;
+          }
+          const uint32_t cm = __ballot_sync(0xffffffffu, cond);
+          if (cm) f = (int32_t)(g + (uint32_t)(__ffs(cm) - 1));   // 1-based depth = m + 1 = i
         }
-        const uint32_t cm = __ballot_sync(0xffffffffu, cond);
-        if (cm) f = (int32_t)(g + (uint32_t)(__ffs(cm) - 1));   // 1-based depth = m + 1 = i
-        carry_flag = __shfl_sync(0xffffffffu, fl, 31);
+        carry_flag = (flm >> 31) & 1u;
       }
       if (L < 32) {
         k = g + (uint32_t)L;
