@@ -382,9 +382,12 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
     const uint32_t id = scratch_register(kp, valid, key_of(S), seg, lane, created);
     if (valid && id) {
       kp.id_of_block[blk0 + i] = id;
-      // APC first-occurrence guess (P0, tag 0); the creator needs no read-before-atomic
+      // Round-0 state.  APC / USER_ISOLATION need the exact first occurrence (they finish in one
+      // pass): seq-min over all occurrences.  For SOLIDARITY it is only the Jacobi starting
+      // guess, so the creator's seq' suffices and the other occurrences skip the dependent
+      // read-before-atomic on the (often hot) staged state.
       if (created) atomicMin(&kp.hot[id].v[0], guess);
-      else atomic_min_u64(&kp.hot[id].v[0], guess);
+      else if (POLICY != SOLID_POLICY_SOLIDARITY) atomic_min_u64(&kp.hot[id].v[0], guess);
     }
   }
   return bad;
@@ -954,7 +957,7 @@ static void launch_eval(solid_ctx* c, uint32_t t, cudaStream_t s) {
 }
 
 static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
-  k_commit<<<dim3(64, kNSeg), 256, 0, s>>>(c->kp, c->tf, mode);   // ~1 key id per thread
+  k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, c->tf, mode);
 }
 
 extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b, solid_result* out,
