@@ -19,6 +19,7 @@
 // Sequence tags.  Every staged value is a u64 (tag << 32 | seq') with tag = ~(E*4096 + sub),
 // seq' = batch position + 1, sub = 0 (round-0 guess), t (round t), 4095 (index snapshot).  atomicMin
 // keeps the EARLIEST request of the newest tag, so stale rounds and batches never need clearing.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -32,6 +33,8 @@
 #include "solid_math.cuh"
 
 namespace solid {
+
+namespace cg = cooperative_groups;
 
 constexpr int kNSeg = 128;            // id-allocation segments (spread the allocation atomics)
 constexpr uint32_t kSubSnap = 4095;
@@ -56,7 +59,7 @@ static_assert(sizeof(Hot) == 32 && sizeof(Cold) == 24, "layout");
 
 struct DevStatus {
   uint32_t err;
-  uint32_t pad;
+  uint32_t conv;                         // converged round (0 = not converged)
   unsigned long long new_entries;        // entries claimed by k_commit
   unsigned long long new_flags;          // sharer writes on index (snapshot) entries
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
@@ -382,12 +385,11 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
     const uint32_t id = scratch_register(kp, valid, key_of(S), seg, lane, created);
     if (valid && id) {
       kp.id_of_block[blk0 + i] = id;
-      // Round-0 state.  APC / USER_ISOLATION need the exact first occurrence (they finish in one
-      // pass): seq-min over all occurrences.  For SOLIDARITY it is only the Jacobi starting
-      // guess, so the creator's seq' suffices and the other occurrences skip the dependent
-      // read-before-atomic on the (often hot) staged state.
+      // Round-0 state: the exact first occurrence (seq-min over all occurrences).  APC and
+      // USER_ISOLATION finish from it in one pass; for SOLIDARITY it is the Jacobi starting
+      // point (a worse start, e.g. the creator's seq', costs extra heavy rounds on C2).
       if (created) atomicMin(&kp.hot[id].v[0], guess);
-      else if (POLICY != SOLID_POLICY_SOLIDARITY) atomic_min_u64(&kp.hot[id].v[0], guess);
+      else atomic_min_u64(&kp.hot[id].v[0], guess);
     }
   }
   return bad;
@@ -452,19 +454,13 @@ __device__ __forceinline__ uint32_t iso_first(const KParams& kp, uint32_t id, in
 }
 
 template <int POLICY>
-__global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (j >= kp.n) return;
-  // all per-request loads are issued before the convergence test so their latencies overlap
-  const uint32_t more = (t >= 2) ? kp.st->changed[t - 1] : 1u;
+__device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint64_t j, int lane) {
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
   const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
   const uint32_t u = kp.users[j];
   const bool enf = (POLICY == SOLID_POLICY_SOLIDARITY) && (kp.enforce ? kp.enforce[j] != 0 : true);
   const uint4 prev =
       (POLICY == SOLID_POLICY_SOLIDARITY && t >= 2) ? kp.dec[j] : make_uint4(0, ~0u, 0, 0);
-  if (more == 0) return;                                 // converged in an earlier round
   if (o1 < o0) return;
   const uint64_t nb = (o1 - o0) >> 4;
   if (nb > kp.max_blocks) return;
@@ -654,6 +650,34 @@ __global__ void __launch_bounds__(256) k_eval(KParams kp, uint32_t t) {
     res.bits = (r > 0 ? 1u : 0u) | ((n > 0 && r == n) ? 2u : 0u) | (f >= 0 ? 4u : 0u) |
                ((f >= 0 && (uint32_t)f < kk) ? 8u : 0u) | (flagd > 0 ? 16u : 0u);
     kp.out[j] = res;
+  }
+}
+
+// The resolver: all rounds in one persistent cooperative launch (grid = resident CTAs).  Warps
+// stride over the requests; between rounds a grid-wide barrier and a gpu-scope fence (which also
+// invalidates L1, so the next round sees every atomic of this one).  Stops at the first round
+// t >= 2 whose decisions all equal round t-1's, or after t_max.
+template <int POLICY>
+__global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = 1; t <= t_max; ++t) {
+    for (uint64_t j = w0; j < kp.n; j += nw) eval_request<POLICY>(kp, t, j, lane);
+    if (POLICY != SOLID_POLICY_SOLIDARITY) {         // exact in one pass
+      if (grid.thread_rank() == 0) kp.st->conv = 1;
+      return;
+    }
+    __threadfence();
+    grid.sync();
+    __threadfence();
+    const uint32_t ch = *(volatile uint32_t*)&kp.st->changed[t];
+    const uint32_t er = *(volatile uint32_t*)&kp.st->err;
+    if ((t >= 2 && ch == 0) || er) {
+      if (grid.thread_rank() == 0) kp.st->conv = (t >= 2 && ch == 0) ? t : 0;
+      return;
+    }
   }
 }
 
@@ -946,14 +970,23 @@ static unsigned grid_for_warps(uint64_t warps) {
   return (unsigned)((warps * 32 + 255) / 256);
 }
 
-static void launch_eval(solid_ctx* c, uint32_t t, cudaStream_t s) {
-  const unsigned grid = grid_for_warps(c->kp.n);
-  switch (c->cfg.policy) {
-    case SOLID_POLICY_APC: k_eval<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(c->kp, t); break;
-    case SOLID_POLICY_USER_ISOLATION:
-      k_eval<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(c->kp, t); break;
-    default: k_eval<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(c->kp, t); break;
+// Persistent cooperative launch of the resolver: one CTA per resident slot (all co-resident).
+static solid_status launch_resolve(solid_ctx* ctx, cudaStream_t s) {
+  const void* fn;
+  switch (ctx->cfg.policy) {
+    case SOLID_POLICY_APC: fn = (const void*)k_resolve<SOLID_POLICY_APC>; break;
+    case SOLID_POLICY_USER_ISOLATION: fn = (const void*)k_resolve<SOLID_POLICY_USER_ISOLATION>; break;
+    default: fn = (const void*)k_resolve<SOLID_POLICY_SOLIDARITY>; break;
   }
+  int per_sm = 0, sms = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+  const uint64_t need = (ctx->kp.n * 32 + 255) / 256;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)per_sm * sms, need));
+  uint32_t tmax = kMaxRounds;
+  void* args[] = {(void*)&ctx->kp, (void*)&tmax};
+  CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, s));
+  return SOLID_OK;
 }
 
 static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
@@ -1029,45 +1062,23 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
     ctx->launches = 1;
   }
   CK(cudaEventRecord(ctx->ev[1], s));
-  if (n && ctx->cfg.policy != SOLID_POLICY_SOLIDARITY) {
-    CK(cudaEventRecord(ctx->ev[4], s));
-    launch_eval(ctx, 1, s);      // exact in one pass: round-0 first occurrences are final
-    CK(cudaEventRecord(ctx->ev[5], s));
-    CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[4], s));
+  if (n) {
+    solid_status rc = launch_resolve(ctx, s);
+    if (rc != SOLID_OK) return rc;
     ctx->launches += 1;
-    ctx->tf = 0;
-    rounds = 1;
-    CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-  } else if (n) {
-    // Jacobi rounds until no decision changes.  Rounds are enqueued ahead in
-    // chunks; a round whose predecessor saw no change exits at once.
-    uint32_t t = 1, conv = 0, chunk = 4;
-    while (!conv) {
-      for (uint32_t q = 0; q < chunk && t <= kMaxRounds; ++q, ++t) {
-        if (t == 1) CK(cudaEventRecord(ctx->ev[4], s));
-        launch_eval(ctx, t, s);
-        if (t == 1) CK(cudaEventRecord(ctx->ev[5], s));
-        ctx->launches += 1;
-      }
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      if (ctx->st_host->err) break;
-      for (uint32_t q = 2; q < t; ++q)
-        if (ctx->st_host->changed[q] == 0) {
-          conv = q;
-          break;
-        }
-      if (!conv && t > kMaxRounds)
-        return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
-      chunk = std::min<uint32_t>(chunk * 2, 64);
-    }
-    ctx->tf = conv;
-    rounds = conv;
+  }
+  CK(cudaEventRecord(ctx->ev[5], s));
+  CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (n && !ctx->st_host->err && ctx->st_host->conv == 0)
+    return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
+  if (ctx->cfg.policy == SOLID_POLICY_SOLIDARITY) {
+    ctx->tf = ctx->st_host->conv;
+    rounds = ctx->st_host->conv;
   } else {
-    CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    ctx->tf = 0;              // APC / USER_ISOLATION commit the round-0 first occurrences
+    rounds = n ? 1 : 0;
   }
   CK(cudaEventRecord(ctx->ev[2], s));
   if (ctx->st_host->err) {
