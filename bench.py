@@ -190,7 +190,7 @@ def main():
     nblk = stream_np.n_blocks()
     dev = torch.device("cuda", local)
     d = P.to_device(stream_np, dev)
-    idx = P.Index("solidarity", capacity_blocks=max(2 * nblk // 10, 1 << 20),
+    idx = P.Index("solidarity", capacity_blocks=max(nblk // 6, 1 << 20),   # C2: ~0.92 M new entries
                   max_batch_tokens=stream_np.n_tokens + 64, max_batch_requests=N,
                   seed=SEED, device=local)
     out = torch.empty((N, 6), dtype=torch.int32, device=dev)

@@ -296,89 +296,65 @@ __device__ __forceinline__ uint32_t scratch_find(const KParams& kp, uint64_t key
 // Forward-exponent chain:
 //   S[b] = sum_{t<=b} M^(t-1) * (h_t + sigma)   — a prefix SUM: warp shfl scan + scalar carry.
 // ---------------------------------------------------------------------------------------------
-// Token staging through shared memory.  A warp copies the 16-byte chunks of one 32-block group
-// with cp.async (LDGSTS: 512 contiguous bytes per warp instruction, no register staging) into
-// 80-byte rows (64 B block + 16 B pad), so the per-lane LDS.128 reads of a row are bank-conflict
-// free.  Two stages per warp: the next group's copies are in flight while this group hashes and
-// registers.  A misaligned request (SH != 0) needs a 5th chunk per block: row l+1, column 0.
-constexpr int kRowBytes = 80;
-constexpr int kStageBytes = 33 * kRowBytes;
-constexpr int kWarpsPerCta = 8;
-
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// Token loads: each lane loads its own 64-byte block with 16-byte non-coherent loads (4 when
+// the request is 16-byte aligned, the aligned 20-word window when it is not; SH is warp-uniform),
+// one group ahead: the next group's loads are in flight while this group hashes and registers.
+// (A cp.async staging through bank-conflict-free shared rows measured slower: 323 vs 290 us on
+// C2 — this kernel is bound by the registration latency, not by the token loads.)
+__device__ __forceinline__ uint4 ldg_v4(const uint32_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
 }
 
 template <int SH>
-__device__ __forceinline__ void stage_group(uint32_t sdst, const uint32_t* a0, uint32_t G,
-                                            uint32_t nblk, int lane) {
-  const uint32_t nch = 4 * nblk + (SH ? 1 : 0);
-  const uint32_t* src = a0 + (uint64_t)512 * G;          // 128 chunks of 4 words per group
-  for (uint32_t c = lane; c < nch; c += 32)
-    cp_async16(sdst + (c >> 2) * kRowBytes + (c & 3) * 16, src + 4 * c);
-  cp_async_commit();
-}
-
-// h = sum_i (tok_i + 1) K_i mod p from the staged row; the "+1" is folded into kp.ksum_*.
-template <int SH>
-__device__ __forceinline__ uint64_t hash_row(const uint8_t* row, const KParams& kp,
-                                             uint32_t& bad) {
-  uint32_t w[20];
+struct BlockWords {
+  static constexpr int W = SH ? 20 : 16;
+  uint32_t w[W];
+  __device__ __forceinline__ void load(const uint32_t* p) {
+    const uint32_t* a = p - SH;
 #pragma unroll
-  for (int q = 0; q < (SH ? 5 : 4); ++q) {
-    const uint4 v = *reinterpret_cast<const uint4*>(row + (q < 4 ? 16 * q : kRowBytes));
-    w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    for (int q = 0; q < W / 4; ++q) {
+      const uint4 v = ldg_v4(a + 4 * q);
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
   }
-  uint64_t lo = kp.ksum_lo, hi = kp.ksum_hi;
-  uint32_t orv = 0;
+  // h = sum_i (tok_i + 1) K_i mod p; the "+1" is folded into kp.ksum_*.
+  __device__ __forceinline__ uint64_t hash(const KParams& kp, uint32_t& bad) const {
+    uint64_t lo = kp.ksum_lo, hi = kp.ksum_hi;
+    uint32_t orv = 0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint32_t t = w[i + SH];
-    orv |= t;
-    lo += (uint64_t)t * kp.klo[i];
-    hi += (uint64_t)t * kp.khi[i];
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t t = w[i + SH];
+      orv |= t;
+      lo += (uint64_t)t * kp.klo[i];
+      hi += (uint64_t)t * kp.khi[i];
+    }
+    bad |= orv >> 20;
+    // lo + hi*2^32 mod p, with hi*2^32 = (hi mod 2^29)*2^32 + (hi >> 29)*2^61 == ... + (hi >> 29)
+    return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
   }
-  bad |= orv >> 20;
-  // lo + hi*2^32 mod p, with hi*2^32 = (hi mod 2^29)*2^32 + (hi >> 29)*2^61 == ... + (hi >> 29)
-  return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
-}
+};
 
 template <int POLICY, int SH>
 __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uint64_t j, int lane,
                                                           const uint32_t* base, uint32_t n,
                                                           uint64_t blk0, uint32_t u,
-                                                          uint32_t seg, uint8_t* stages) {
+                                                          uint32_t seg) {
   const uint64_t sig = (POLICY == SOLID_POLICY_USER_ISOLATION) ? sigma_of(kp.seed, u) : 0;
   const unsigned long long guess =
       ((unsigned long long)tag_of(kp.epoch, 0) << 32) | (unsigned long long)(j + 1);
-  const uint32_t* a0 = base - SH;                         // 16-byte aligned
-  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(stages);
-  const uint32_t ngroups = (n + 31) / 32;
   uint64_t carry = 0;
   uint32_t bad = 0;
-  if (ngroups) stage_group<SH>(s0, a0, 0, min(n, 32u), lane);
-  for (uint32_t G = 0; G < ngroups; ++G) {
-    const uint32_t g = 32 * G;
-    if (G + 1 < ngroups) {
-      stage_group<SH>(s0 + ((G + 1) & 1) * kStageBytes, a0, G + 1, min(n - g - 32, 32u), lane);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncwarp();
+  BlockWords<SH> cur, nxt;
+  if ((uint32_t)lane < n) cur.load(base + (uint64_t)kBS * lane);
+  for (uint32_t g = 0; g < n; g += 32) {
     const uint32_t i = g + lane;
     const bool valid = i < n;
+    if (i + 32 < n) nxt.load(base + (uint64_t)kBS * (i + 32));       // prefetch next group
     uint64_t term = 0;
-    if (valid) {
-      const uint8_t* row = stages + (G & 1) * kStageBytes + lane * kRowBytes;
-      term = mulmod(addmod(hash_row<SH>(row, kp, bad), sig), kp.mpow[i]);
-    }
-    __syncwarp();                                         // stage G&1 may be refilled next
+    if (valid) term = mulmod(addmod(cur.hash(kp, bad), sig), kp.mpow[i]);
     const uint64_t S = addmod(warp_scan_addmod(term, lane), carry);
     carry = __shfl_sync(0xffffffffu, S, 31);
     bool created = false;
@@ -391,15 +367,14 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
       if (created) atomicMin(&kp.hot[id].v[0], guess);
       else atomic_min_u64(&kp.hot[id].v[0], guess);
     }
+    cur = nxt;
   }
   return bad;
 }
 
 template <int POLICY>
 __global__ void __launch_bounds__(256) k_hash_register(KParams kp) {
-  __shared__ __align__(16) uint8_t stage_mem[kWarpsPerCta][2 * kStageBytes];
   const int lane = threadIdx.x & 31;
-  uint8_t* stages = stage_mem[threadIdx.x >> 5];
   const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= kp.n) return;
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
@@ -424,10 +399,10 @@ __global__ void __launch_bounds__(256) k_hash_register(KParams kp) {
   const uint32_t* base = kp.tokens + o0;
   uint32_t bad;
   switch (((uintptr_t)base >> 2) & 3) {
-    case 0: bad = hash_register_request<POLICY, 0>(kp, j, lane, base, n, blk0, u, seg, stages); break;
-    case 1: bad = hash_register_request<POLICY, 1>(kp, j, lane, base, n, blk0, u, seg, stages); break;
-    case 2: bad = hash_register_request<POLICY, 2>(kp, j, lane, base, n, blk0, u, seg, stages); break;
-    default: bad = hash_register_request<POLICY, 3>(kp, j, lane, base, n, blk0, u, seg, stages); break;
+    case 0: bad = hash_register_request<POLICY, 0>(kp, j, lane, base, n, blk0, u, seg); break;
+    case 1: bad = hash_register_request<POLICY, 1>(kp, j, lane, base, n, blk0, u, seg); break;
+    case 2: bad = hash_register_request<POLICY, 2>(kp, j, lane, base, n, blk0, u, seg); break;
+    default: bad = hash_register_request<POLICY, 3>(kp, j, lane, base, n, blk0, u, seg); break;
   }
   if (__any_sync(0xffffffffu, bad != 0) && lane == 0) set_err(kp.st, ERR_TOKEN);
 }
