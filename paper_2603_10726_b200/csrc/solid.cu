@@ -665,41 +665,65 @@ __global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) 
 // every claimed slot was EMPTY before, so emptying it again restores the previous probe chains.
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mode) {
+  constexpr int U = 4;                 // ids per thread, staged so all loads are in flight at once
   const uint32_t seg = blockIdx.y;
   const uint32_t cnt = min(kp.seg_cnt[seg], kp.seg_cap);
   const int W = (int)(tf & 1);
   const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
   uint32_t c_new = 0, c_flag = 0;
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * blockDim.x) {
-    const uint32_t id = seg * kp.seg_cap + x + 1;
-    const ulonglong2 pw = ldw128(&kp.hot[id].v[2 * W]);
-    const unsigned long long iv = pw.x, fv = pw.y;
-    const uint32_t itag = (uint32_t)(iv >> 32);
-    if (itag == tag) {
-      ++c_new;
-      Cold* c = kp.cold + id;
-      if (mode == 1) {
-        const uint64_t key = c->key;
-        const uint32_t owner = kp.users[(uint32_t)iv - 1u];
-        const uint32_t sharer = ((uint32_t)(fv >> 32) == tag) ? kp.users[(uint32_t)fv - 1u] : kNone;
-        const ulonglong2 val = make_ulonglong2(key, (unsigned long long)owner |
-                                                        ((unsigned long long)sharer << 32));
-        uint64_t p = key & kp.tmask;
-        for (;;) {
-          const ulonglong2 old = atomic_cas128(&kp.tab[p], make_ulonglong2(0ull, 0ull), val);
-          if (old.x == 0 || old.x == key) break;
-          p = (p + 1) & kp.tmask;
-        }
-        c->psl = (uint32_t)p;
-      } else {
-        kp.tab[c->psl] = make_ulonglong2(0ull, 0ull);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t x0 = blockIdx.x * blockDim.x + threadIdx.x; x0 < cnt; x0 += U * stride) {
+    ulonglong2 pw[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const uint32_t x = x0 + q * stride;
+      pw[q] = x < cnt ? ldw128(&kp.hot[seg * kp.seg_cap + x + 1].v[2 * W])
+                      : make_ulonglong2(~0ull, ~0ull);
+    }
+    uint64_t key[U];
+    uint32_t who[U], sharer[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const uint32_t id = seg * kp.seg_cap + x0 + q * stride + 1;
+      const uint32_t itag = (uint32_t)(pw[q].x >> 32);
+      const bool ins = itag == tag, flg = itag == tagS && (uint32_t)(pw[q].y >> 32) == tag;
+      key[q] = 0;
+      who[q] = kNone;
+      sharer[q] = kNone;
+      if (ins) {
+        key[q] = kp.cold[id].key;
+        who[q] = kp.users[(uint32_t)pw[q].x - 1u];
+        if ((uint32_t)(pw[q].y >> 32) == tag) sharer[q] = kp.users[(uint32_t)pw[q].y - 1u];
+      } else if (flg) {
+        who[q] = kp.users[(uint32_t)pw[q].y - 1u];
       }
-    } else if (itag == tagS && (uint32_t)(fv >> 32) == tag) {
-      ++c_flag;
-      const uint32_t who = kp.users[(uint32_t)fv - 1u];
-      uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
-      if (mode == 1) atomicCAS(sharer_word, kNone, who);
-      else atomicCAS(sharer_word, who, kNone);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const uint32_t id = seg * kp.seg_cap + x0 + q * stride + 1;
+      const uint32_t itag = (uint32_t)(pw[q].x >> 32);
+      if (itag == tag) {
+        ++c_new;
+        Cold* c = kp.cold + id;
+        if (mode == 1) {
+          const ulonglong2 val =
+              make_ulonglong2(key[q], (unsigned long long)who[q] | ((unsigned long long)sharer[q] << 32));
+          uint64_t p = key[q] & kp.tmask;
+          for (;;) {
+            const ulonglong2 old = atomic_cas128(&kp.tab[p], make_ulonglong2(0ull, 0ull), val);
+            if (old.x == 0 || old.x == key[q]) break;
+            p = (p + 1) & kp.tmask;
+          }
+          c->psl = (uint32_t)p;
+        } else {
+          kp.tab[c->psl] = make_ulonglong2(0ull, 0ull);
+        }
+      } else if (itag == tagS && (uint32_t)(pw[q].y >> 32) == tag) {
+        ++c_flag;
+        uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
+        if (mode == 1) atomicCAS(sharer_word, kNone, who[q]);
+        else atomicCAS(sharer_word, who[q], kNone);
+      }
     }
   }
   for (int o = 16; o; o >>= 1) {
@@ -965,7 +989,7 @@ static solid_status launch_resolve(solid_ctx* ctx, cudaStream_t s) {
 }
 
 static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
-  k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, c->tf, mode);
+  k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, c->tf, mode);   // 4 staged ids per thread
 }
 
 extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b, solid_result* out,
