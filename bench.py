@@ -319,6 +319,7 @@ def main():
             "clocks": clocks,
             "phases_ms_median": {k: statistics.median(v) for k, v in phase.items() if v},
             "resolver_rounds": rounds[-1] if rounds else None,
+            "resolver_round_us": [round(x, 1) for x in stats["round_us"]],
             "step_ms": ms,
             "result_summary": {"reused_blocks": int(res["reused"].sum()),
                                "diverted": int(((res["bits"] & 4) > 0).sum()),

@@ -106,7 +106,8 @@ typedef struct {
   uint64_t algorithmic_bytes;    /* DESIGN.md §5 formula for the last batch                  */
   uint64_t last_kernel_launches; /* kernels this library launched for the last batch         */
   float ms_hash_kernel;          /* device time of k_hash_register alone (last batch)        */
-  float ms_round_first;          /* device time of the first resolver round (last batch)     */
+  float ms_round_first;          /* device time of the resolver kernel (last batch)          */
+  float round_us[8];             /* device time of resolver rounds 1..8 (globaltimer)        */
 } solid_stats_t;
 
 uint32_t solid_abi_version(void);

@@ -62,7 +62,7 @@ class _Stats(ctypes.Structure):
                 ("ms_resolve", ctypes.c_float), ("ms_commit", ctypes.c_float),
                 ("algorithmic_bytes", ctypes.c_uint64),
                 ("last_kernel_launches", ctypes.c_uint64), ("ms_hash_kernel", ctypes.c_float),
-                ("ms_round_first", ctypes.c_float)]
+                ("ms_round_first", ctypes.c_float), ("round_us", ctypes.c_float * 8)]
 
 
 _lib = None
@@ -200,7 +200,9 @@ class Index:
     def stats(self) -> dict:
         s = _Stats()
         self._check(self.lib.solid_stats(self.h, ctypes.byref(s)))
-        return {name: getattr(s, name) for name, _ in _Stats._fields_}
+        d = {name: getattr(s, name) for name, _ in _Stats._fields_}
+        d["round_us"] = list(d["round_us"])
+        return d
 
     def dump(self) -> np.ndarray:
         n = ctypes.c_uint64()

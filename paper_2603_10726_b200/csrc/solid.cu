@@ -63,6 +63,7 @@ struct DevStatus {
   unsigned long long new_entries;        // entries claimed by k_commit
   unsigned long long new_flags;          // sharer writes on index (snapshot) entries
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
+  unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t changed[kMaxRounds + 2];
 };
 
@@ -101,6 +102,12 @@ __host__ __device__ __forceinline__ uint32_t tag_of(uint32_t epoch, uint32_t sub
 }
 
 __device__ __forceinline__ void set_err(DevStatus* st, uint32_t bits) { atomicOr(&st->err, bits); }
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Weak (L1-cacheable) loads kept in program order.  Used where a stale value is safe: table
 // slots only move stale -> live within a batch, staged values only decrease, and L1 is
@@ -638,6 +645,7 @@ __global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) 
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  if (grid.thread_rank() == 0) kp.st->round_ns[0] = globaltimer_ns();
   for (uint32_t t = 1; t <= t_max; ++t) {
     for (uint64_t j = w0; j < kp.n; j += nw) eval_request<POLICY>(kp, t, j, lane);
     if (POLICY != SOLID_POLICY_SOLIDARITY) {         // exact in one pass
@@ -647,6 +655,7 @@ __global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) 
     __threadfence();
     grid.sync();
     __threadfence();
+    if (grid.thread_rank() == 0 && t <= 16) kp.st->round_ns[t] = globaltimer_ns();
     const uint32_t ch = *(volatile uint32_t*)&kp.st->changed[t];
     const uint32_t er = *(volatile uint32_t*)&kp.st->err;
     if ((t >= 2 && ch == 0) || er) {
@@ -1134,6 +1143,10 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   ctx->live += h.new_entries;
   S.live_entries = ctx->live;
   S.last_rounds = ctx->rounds;
+  for (int q = 0; q < 8; ++q)
+    S.round_us[q] = (q < (int)ctx->rounds && q < 16 && h.round_ns[q + 1] > h.round_ns[0])
+                        ? (float)((h.round_ns[q + 1] - h.round_ns[q]) * 1e-3)
+                        : 0.f;
   uint64_t distinct = 0;
   for (int q = 0; q < kNSeg; ++q) distinct += std::min<uint32_t>(ctx->seg_host[q], ctx->seg_cap);
   S.last_distinct_keys = (uint32_t)std::min<uint64_t>(distinct, 0xFFFFFFFFull);
