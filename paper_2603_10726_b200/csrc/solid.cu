@@ -88,7 +88,6 @@ struct KParams {
   ulonglong2* tab;                 // the index {key, owner | sharer << 32}
   uint64_t tmask;
   uint32_t* id_of_block;           // per block: id of its Shared (USER_ISOLATION: U) key
-  unsigned long long* key_of_block;  // per block: its Shared key (isolated keys derive from it)
   uint32_t* iso_id;                // per block: id of its isolated key (valid for dec.f)
   uint64_t slot_cap;
   uint4* dec;
@@ -366,9 +365,7 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
     const uint64_t S = addmod(warp_scan_addmod(term, lane), carry);
     carry = __shfl_sync(0xffffffffu, S, 31);
     bool created = false;
-    const uint64_t key = key_of(S);
-    if (valid && POLICY == SOLID_POLICY_SOLIDARITY) kp.key_of_block[blk0 + i] = key;
-    const uint32_t id = scratch_register(kp, valid, key, seg, lane, created);
+    const uint32_t id = scratch_register(kp, valid, key_of(S), seg, lane, created);
     if (valid && id) {
       kp.id_of_block[blk0 + i] = id;
       // Round-0 state: the exact first occurrence (seq-min over all occurrences).  APC and
@@ -427,7 +424,7 @@ __device__ __forceinline__ uint32_t owner_from(const KParams& kp, uint32_t id, u
 
 __device__ __forceinline__ uint64_t iso_key(const KParams& kp, uint64_t blk, uint32_t i,
                                             uint64_t sig, uint64_t gf) {
-  const uint64_t S = chain_of(kp.key_of_block[blk]);
+  const uint64_t S = chain_of(kp.cold[kp.id_of_block[blk]].key);
   const uint64_t d = submod(kp.gtab[i + 1], gf);   // G[b] - G[f], b = i + 1
   return key_of(addmod(S, mulmod(sig, d)));
 }
@@ -801,7 +798,6 @@ struct solid_ctx {
   Cold* cold = nullptr;
   uint64_t idcap = 0;
   uint32_t* id_of_block = nullptr;
-  unsigned long long* key_of_block = nullptr;
   uint32_t* iso_id = nullptr;
   uint64_t slot_cap = 0;
   uint4* dec = nullptr;
@@ -866,7 +862,6 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->hot);
   cudaFree(c->cold);
   cudaFree(c->id_of_block);
-  cudaFree(c->key_of_block);
   cudaFree(c->iso_id);
   cudaFree(c->dec);
   cudaFree(c->seg_cnt);
@@ -928,7 +923,6 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
             alloc((void**)&ctx->hot, ctx->idcap * sizeof(Hot)) &&
             alloc((void**)&ctx->cold, ctx->idcap * sizeof(Cold)) &&
             alloc((void**)&ctx->id_of_block, ctx->slot_cap * sizeof(uint32_t)) &&
-            alloc((void**)&ctx->key_of_block, ctx->slot_cap * sizeof(unsigned long long)) &&
             alloc((void**)&ctx->iso_id, ctx->slot_cap * sizeof(uint32_t)) &&
             alloc((void**)&ctx->dec, cfg->max_batch_requests * sizeof(uint4)) &&
             alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(uint32_t)) &&
@@ -1051,7 +1045,6 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   kp.tab = ctx->tab;
   kp.tmask = ctx->tcap - 1;
   kp.id_of_block = ctx->id_of_block;
-  kp.key_of_block = ctx->key_of_block;
   kp.iso_id = ctx->iso_id;
   kp.slot_cap = ctx->slot_cap;
   kp.dec = ctx->dec;
