@@ -161,14 +161,6 @@ __device__ __forceinline__ uint32_t gs_first(unsigned long long p0, unsigned lon
   return s;
 }
 
-// Jacobi view (round t-1's complete values only): seq' of the first request, 0 = snapshot, kNone.
-__device__ __forceinline__ uint32_t jacobi_first(unsigned long long v, uint32_t seqp,
-                                                 uint32_t tagR, uint32_t tagS) {
-  const uint32_t tg = (uint32_t)(v >> 32);
-  if (tg == tagS) return 0;
-  return (tg == tagR && (uint32_t)v < seqp) ? (uint32_t)v : kNone;
-}
-
 // ---------------------------------------------------------------------------------------------
 // Index probe: linear probing over 16-byte slots {key, owner | sharer << 32}; 0 = empty.
 // ---------------------------------------------------------------------------------------------
@@ -429,10 +421,12 @@ __device__ __forceinline__ uint64_t iso_key(const KParams& kp, uint64_t blk, uin
   return key_of(addmod(S, mulmod(sig, d)));
 }
 
-__device__ __forceinline__ uint32_t iso_first(const KParams& kp, uint32_t id, int R, uint32_t seqp,
-                                              uint32_t tagR, uint32_t tagW, uint32_t tagS) {
+// Gauss-Seidel visibility of an isolated key: round t-1's value (P[R]) or a value already
+// published this round (P[W], whose tags are snapshot, t, or older-and-larger).
+__device__ __forceinline__ bool iso_visible(const KParams& kp, uint32_t id, int R,
+                                            unsigned long long limR, unsigned long long limW) {
   const Hot* h = kp.hot + id;
-  return gs_first(ldw64(&h->v[0]), ldw64(&h->v[2]), R, seqp, tagR, tagW, tagS);
+  return ldw64(&h->v[2 * R]) < limR || ldw64(&h->v[2 - 2 * R]) < limW;
 }
 
 template <int POLICY>
@@ -460,13 +454,17 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
     iso_pre_id = kp.iso_id[blk0 + (uint32_t)fprev + lane];
 
   // ---- a5: first miss k (warp ballot) and barrier scan f over the Shared chain ----
-  // Blocks are walked 128 at a time: the ids and staged pairs P[R] = {first inserter, first
-  // flagger} of 4 groups of 32 are in flight together, then evaluated group by group.
+  // During round t, P[R] holds only the snapshot tag, round t-1's tag and older (numerically
+  // larger) tags, so "visible to request seqp" is one 64-bit compare v < limR = tagR<<32 | seqp
+  // (snapshot values carry the smallest tag and always pass); likewise "flagged".  Blocks are
+  // walked 128 at a time: ids and P[R] pairs of 4 groups of 32 are in flight together.
+  const unsigned long long limR = ((unsigned long long)tagR << 32) | seqp;
+  const unsigned long long limW = ((unsigned long long)tagW << 32) | seqp;
   uint32_t k = n;
   int32_t f = -1;
   bool carry_flag = false;    // flagged(index g-1) from the previous group
   bool walked = false;
-  uint32_t iso_pre_first = kNone;
+  bool iso_pre_vis = false;
   for (uint32_t base = 0; base <= n && !walked; base += 128) {
     uint32_t idq[4];
     ulonglong2 pq[4];
@@ -476,7 +474,7 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
       idq[q] = i < n ? kp.id_of_block[blk0 + i] : 0u;
     }
     if (POLICY == SOLID_POLICY_SOLIDARITY && base == 0 && fprev >= 1 && (uint32_t)fprev + lane < n)
-      iso_pre_first = iso_first(kp, iso_pre_id, R, seqp, tagR, tagW, tagS);
+      iso_pre_vis = iso_visible(kp, iso_pre_id, R, limR, limW);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t i = base + 32 * q + lane;
@@ -487,15 +485,10 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
     for (int q = 0; q < 4; ++q) {
       const uint32_t g = base + 32 * q;
       if (g > n) break;
-      const uint32_t i = g + lane;
-      const bool valid = i < n;
-      const uint32_t id = idq[q];
-      const uint32_t first = valid ? jacobi_first(pq[q].x, seqp, tagR, tagS) : kNone;
-      const bool vis = first != kNone;
-      const bool fl = valid && POLICY == SOLID_POLICY_SOLIDARITY &&
-                      jacobi_first(pq[q].y, seqp, tagR, tagS) != kNone;
+      const bool vis = pq[q].x < limR;                  // invalid lanes hold ~0: not visible
+      const bool fl = POLICY == SOLID_POLICY_SOLIDARITY && pq[q].y < limR;
       const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
-      const int L = inv ? __ffs(inv) - 1 : 32;         // first invisible lane in this group
+      const int L = inv ? __ffs(inv) - 1 : 32;          // first invisible lane in this group
       if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
         // lane evaluates the barrier condition for index m = i - 1 (needs flagged(m) and the
         // owner of the NEXT entry i): stop at m iff flagged(m) and not (i visible and
@@ -506,7 +499,9 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
           if (lane == 0) pf = carry_flag;
           bool cond = false;
           if (pf && lane <= L && !(g == 0 && lane == 0)) {
-            const bool pass = vis && owner_from(kp, id, first) == u;
+            const uint32_t first =
+                ((uint32_t)(pq[q].x >> 32) == tagS) ? 0u : (uint32_t)pq[q].x;
+            const bool pass = vis && owner_from(kp, idq[q], first) == u;
             cond = !pass;
           }
           const uint32_t cm = __ballot_sync(0xffffffffu, cond);
@@ -534,8 +529,8 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
       for (uint32_t g = (uint32_t)f; g < n; g += 32) {
         const uint32_t i = g + lane;
         bool vis = false;
-        if (g == (uint32_t)f) vis = i < n && iso_pre_first != kNone;
-        else if (i < n) vis = iso_first(kp, kp.iso_id[blk0 + i], R, seqp, tagR, tagW, tagS) != kNone;
+        if (g == (uint32_t)f) vis = i < n && iso_pre_vis;
+        else if (i < n) vis = iso_visible(kp, kp.iso_id[blk0 + i], R, limR, limW);
         const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
         if (inv) {
           m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
@@ -559,7 +554,7 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
         bool bvis = false;
         if (valid) {
           kp.iso_id[blk0 + i] = id;
-          bvis = iso_first(kp, id, R, seqp, tagR, tagW, tagS) != kNone;
+          bvis = iso_visible(kp, id, R, limR, limW);
         }
         // lanes not visible through the staged state may still be in the index snapshot; probe
         // them in order, only until the first key that is absent (the walk stops there)
