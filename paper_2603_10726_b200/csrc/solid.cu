@@ -604,7 +604,9 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
   if (POLICY == SOLID_POLICY_SOLIDARITY) {
     const unsigned long long mine = ((unsigned long long)tagW << 32) | (unsigned long long)seqp;
     const uint32_t* ids = (f >= 1) ? kp.iso_id : kp.id_of_block;
-    for (uint32_t i = r + lane; i < n; i += 32) atomic_min_u64(&kp.hot[ids[blk0 + i]].v[2 * W], mine);
+    // fire-and-forget RED: within a round, concurrent inserters of one key are rare (a request
+    // only inserts keys invisible to it), unlike the hot keys of K_A
+    for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.hot[ids[blk0 + i]].v[2 * W], mine);
   }
 
   if (lane == 0) {
@@ -635,7 +637,7 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
 // invalidates L1, so the next round sees every atomic of this one).  Stops at the first round
 // t >= 2 whose decisions all equal round t-1's, or after t_max.
 template <int POLICY>
-__global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) {
+__global__ void __launch_bounds__(256, 5) k_resolve(KParams kp, uint32_t t_max) {
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
