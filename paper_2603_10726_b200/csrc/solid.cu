@@ -65,7 +65,6 @@ struct DevStatus {
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t changed[kMaxRounds + 2];
-  uint32_t next_req[kMaxRounds + 2];     // per-round work counter of the persistent resolver
 };
 
 struct KParams {
@@ -638,20 +637,14 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
 // invalidates L1, so the next round sees every atomic of this one).  Stops at the first round
 // t >= 2 whose decisions all equal round t-1's, or after t_max.
 template <int POLICY>
-__global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) {
+__global__ void __launch_bounds__(256, 5) k_resolve(KParams kp, uint32_t t_max) {
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
+  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   if (grid.thread_rank() == 0) kp.st->round_ns[0] = globaltimer_ns();
-  constexpr uint32_t kChunk = 8;      // requests claimed per atomic: dynamic balance, few atomics
   for (uint32_t t = 1; t <= t_max; ++t) {
-    for (;;) {
-      uint32_t c0 = 0;
-      if (lane == 0) c0 = atomicAdd(&kp.st->next_req[t], kChunk);
-      c0 = __shfl_sync(0xffffffffu, c0, 0);
-      if (c0 >= kp.n) break;
-      const uint64_t c1 = min((uint64_t)c0 + kChunk, kp.n);
-      for (uint64_t j = c0; j < c1; ++j) eval_request<POLICY>(kp, t, j, lane);
-    }
+    for (uint64_t j = w0; j < kp.n; j += nw) eval_request<POLICY>(kp, t, j, lane);
     if (POLICY != SOLID_POLICY_SOLIDARITY) {         // exact in one pass
       if (grid.thread_rank() == 0) kp.st->conv = 1;
       return;
