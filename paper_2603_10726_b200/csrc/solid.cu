@@ -763,6 +763,28 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
   }
 }
 
+// Compact the live index slots (dump): warp-aggregated append.
+__global__ void __launch_bounds__(256) k_compact(const ulonglong2* tab, uint64_t tcap,
+                                                 ulonglong2* out, unsigned long long* cnt,
+                                                 unsigned long long cap) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < tcap;
+       base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    ulonglong2 e = make_ulonglong2(0, 0);
+    if (i < tcap) e = tab[i];
+    const uint32_t m = __ballot_sync(0xffffffffu, e.x != 0);
+    if (!m) continue;
+    unsigned long long b = 0;
+    if (lane == __ffs(m) - 1) b = atomicAdd(cnt, (unsigned long long)__popc(m));
+    b = __shfl_sync(0xffffffffu, b, __ffs(m) - 1);
+    if (e.x) {
+      const unsigned long long o = b + __popc(m & ((1u << lane) - 1u));
+      if (o < cap) out[o] = e;
+    }
+  }
+}
+
 __global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long v) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -1219,12 +1241,26 @@ extern "C" solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
-  std::vector<ulonglong2> h(ctx->tcap);
-  CK(cudaMemcpy(h.data(), ctx->tab, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToHost));
+  // compact the live slots on the device, copy only those
+  const unsigned long long cap_e = ctx->live + 1024;
+  ulonglong2* dbuf = nullptr;
+  unsigned long long* dcnt = nullptr;
+  CK(cudaMalloc(&dbuf, cap_e * sizeof(ulonglong2)));
+  CK(cudaMalloc(&dcnt, sizeof(unsigned long long)));
+  CK(cudaMemset(dcnt, 0, sizeof(unsigned long long)));
+  k_compact<<<2048, 256>>>(ctx->tab, ctx->tcap, dbuf, dcnt, cap_e);
+  CK(cudaGetLastError());
+  unsigned long long hc = 0;
+  CK(cudaMemcpy(&hc, dcnt, sizeof(hc), cudaMemcpyDeviceToHost));
+  std::vector<ulonglong2> h(std::min<unsigned long long>(hc, cap_e));
+  if (!h.empty())
+    CK(cudaMemcpy(h.data(), dbuf, h.size() * sizeof(ulonglong2), cudaMemcpyDeviceToHost));
+  cudaFree(dbuf);
+  cudaFree(dcnt);
+  if (hc > cap_e) return fail(ctx, SOLID_ERR_STATE, "dump: index holds more entries than tracked");
   std::vector<solid_entry> v;
-  v.reserve(ctx->live);
-  for (const auto& e : h)
-    if (e.x) v.push_back(solid_entry{e.x, (uint32_t)e.y, (uint32_t)(e.y >> 32)});
+  v.reserve(h.size());
+  for (const auto& e : h) v.push_back(solid_entry{e.x, (uint32_t)e.y, (uint32_t)(e.y >> 32)});
   std::sort(v.begin(), v.end(), [](const solid_entry& a, const solid_entry& b) { return a.key < b.key; });
   *n_out = v.size();
   const uint64_t m = std::min<uint64_t>(cap, v.size());

@@ -225,3 +225,21 @@ def test_c2_full_size_bench_configuration():
     exp, ed = oracle_run(s, "solidarity")
     got, gd, idx = gpu_run(s, "solidarity")
     assert_same(got, exp, gd, ed, "c2full")
+
+
+def test_c3_full_size_warm_then_timed():
+    """BASELINE configs[2] at full size: 10 000 users, conversations to 8 k tokens, warm phase
+    (~3 M cached blocks) then the timed rounds as one 80 000-request batch."""
+    warm, timed = c3_multiturn()
+    exp, ed = oracle_run([warm, timed], "solidarity")
+    got, gd, _ = gpu_run([warm, timed], "solidarity")
+    assert_same(got, exp, gd, ed, "c3full")
+
+
+def test_c4_full_size():
+    """BASELINE configs[3] at full size: 500 k benign requests + 100 victims x 10 + 1 000
+    colluding attackers x 500 probes, isolation-heavy, one batch."""
+    s = c4_attackers()
+    exp, ed = oracle_run(s, "solidarity")
+    got, gd, _ = gpu_run(s, "solidarity")
+    assert_same(got, exp, gd, ed, "c4full")

@@ -330,9 +330,12 @@ def c4_attackers(benign_users: int = 10000, benign_requests: int = 500_000, vict
                     cands[w] = (cands[w] + 1) % VOCAB
             for ci in range(candidates):
                 p = np.concatenate([t] + true_blocks[:s] + [known[s], cands[ci:ci + 1], sfx16])
-                a = abase + v * colluders_per_victim + (k % colluders_per_victim)
-                items.append((first + (1 - first) * (k + float(rng.random())) / probes_per_victim,
-                              a, p))
+                # every colluder runs the whole probe sequence (500 probes each),
+                # the colluders interleaved with jitter
+                for c in range(colluders_per_victim):
+                    a = abase + v * colluders_per_victim + c
+                    items.append((first + (1 - first) * (k + float(rng.random())) /
+                                  probes_per_victim, a, p))
                 k += 1
     items.sort(key=lambda x: x[0])
     prompts = [it[2].astype(np.uint32) for it in items]
