@@ -732,13 +732,22 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mod
       }
     }
   }
+  // one atomic per CTA (per-warp atomics on one counter serialise on a single L2 slice)
+  __shared__ uint32_t s_new, s_flag;
+  if (threadIdx.x == 0) s_new = s_flag = 0;
+  __syncthreads();
   for (int o = 16; o; o >>= 1) {
     c_new += __shfl_xor_sync(0xffffffffu, c_new, o);
     c_flag += __shfl_xor_sync(0xffffffffu, c_flag, o);
   }
-  if ((threadIdx.x & 31) == 0 && mode == 1 && (c_new | c_flag)) {
-    atomicAdd(&kp.st->new_entries, (unsigned long long)c_new);
-    atomicAdd(&kp.st->new_flags, (unsigned long long)c_flag);
+  if ((threadIdx.x & 31) == 0 && (c_new | c_flag)) {
+    atomicAdd(&s_new, c_new);
+    atomicAdd(&s_flag, c_flag);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && mode == 1 && (s_new | s_flag)) {
+    atomicAdd(&kp.st->new_entries, (unsigned long long)s_new);
+    atomicAdd(&kp.st->new_flags, (unsigned long long)s_flag);
   }
 }
 
@@ -756,11 +765,16 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
     a[4] += (r.bits >> 3) & 1;
     a[5] += 1;
   }
+  __shared__ unsigned long long s_a[6];
+  if (threadIdx.x < 6) s_a[threadIdx.x] = 0;
+  __syncthreads();
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
     for (int o = 16; o; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
-    if ((threadIdx.x & 31) == 0 && a[q]) atomicAdd(&st->sums[q], a[q]);
+    if ((threadIdx.x & 31) == 0 && a[q]) atomicAdd(&s_a[q], a[q]);
   }
+  __syncthreads();
+  if (threadIdx.x < 6 && s_a[threadIdx.x]) atomicAdd(&st->sums[threadIdx.x], s_a[threadIdx.x]);
 }
 
 // Compact the live index slots (dump): warp-aggregated append.
