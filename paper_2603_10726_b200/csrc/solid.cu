@@ -429,20 +429,22 @@ __device__ __forceinline__ bool iso_visible(const KParams& kp, uint32_t id, int 
   return ldw64(&h->v[2 * R]) < limR || ldw64(&h->v[2 - 2 * R]) < limW;
 }
 
+// Evaluates request j in round t; returns true (warp-uniform) if its decision differs from the
+// previous round's (always true in round 1).
 template <int POLICY>
-__device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint64_t j, int lane) {
+__device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint64_t j, int lane) {
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
   const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
   const uint32_t u = kp.users[j];
   const bool enf = (POLICY == SOLID_POLICY_SOLIDARITY) && (kp.enforce ? kp.enforce[j] != 0 : true);
   const uint4 prev =
       (POLICY == SOLID_POLICY_SOLIDARITY && t >= 2) ? kp.dec[j] : make_uint4(0, ~0u, 0, 0);
-  if (o1 < o0) return;
+  if (o1 < o0) return false;
   const uint64_t nb = (o1 - o0) >> 4;
-  if (nb > kp.max_blocks) return;
+  if (nb > kp.max_blocks) return false;
   const uint32_t n = (uint32_t)nb;
   const uint64_t blk0 = o0 >> 4;
-  if (n && blk0 + n > kp.slot_cap) return;
+  if (n && blk0 + n > kp.slot_cap) return false;
   const uint32_t seqp = (uint32_t)(j + 1);
   const int R = (int)((t - 1) & 1), W = (int)(t & 1);
   const uint32_t tagR = tag_of(kp.epoch, t - 1), tagW = tag_of(kp.epoch, t),
@@ -609,15 +611,10 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
     for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.hot[ids[blk0 + i]].v[2 * W], mine);
   }
 
+  const uint4 d = make_uint4(k, (uint32_t)f, r, flagd);
+  const bool changed =
+      t == 1 || prev.x != d.x || prev.y != d.y || prev.z != d.z || prev.w != d.w;
   if (lane == 0) {
-    const uint4 d = make_uint4(k, (uint32_t)f, r, flagd);
-    if (POLICY == SOLID_POLICY_SOLIDARITY) {
-      if (t == 1) {
-        kp.st->changed[1] = 1;
-      } else if (prev.x != d.x || prev.y != d.y || prev.z != d.z || prev.w != d.w) {
-        kp.st->changed[t] = 1;
-      }
-    }
     kp.dec[j] = d;
     const uint32_t kk = (POLICY == SOLID_POLICY_USER_ISOLATION) ? 0u : k;   // no Shared chain
     solid_result res;
@@ -630,6 +627,7 @@ __device__ __forceinline__ void eval_request(const KParams& kp, uint32_t t, uint
                ((f >= 0 && (uint32_t)f < kk) ? 8u : 0u) | (flagd > 0 ? 16u : 0u);
     kp.out[j] = res;
   }
+  return changed;
 }
 
 // The resolver: all rounds in one persistent cooperative launch (grid = resident CTAs).  Warps
@@ -643,8 +641,16 @@ __global__ void __launch_bounds__(256, 5) k_resolve(KParams kp, uint32_t t_max) 
   const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   if (grid.thread_rank() == 0) kp.st->round_ns[0] = globaltimer_ns();
+  __shared__ uint32_t s_changed;
   for (uint32_t t = 1; t <= t_max; ++t) {
-    for (uint64_t j = w0; j < kp.n; j += nw) eval_request<POLICY>(kp, t, j, lane);
+    if (threadIdx.x == 0) s_changed = 0;
+    __syncthreads();
+    bool any = false;
+    for (uint64_t j = w0; j < kp.n; j += nw) any |= eval_request<POLICY>(kp, t, j, lane);
+    // one store per CTA (100k same-address stores would serialise on one L2 slice)
+    if (lane == 0 && any) s_changed = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_changed) kp.st->changed[t] = 1;
     if (POLICY != SOLID_POLICY_SOLIDARITY) {         // exact in one pass
       if (grid.thread_rank() == 0) kp.st->conv = 1;
       return;
