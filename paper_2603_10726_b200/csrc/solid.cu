@@ -659,8 +659,14 @@ __global__ void __launch_bounds__(256, 5) k_resolve(KParams kp, uint32_t t_max) 
     grid.sync();
     __threadfence();
     if (grid.thread_rank() == 0 && t <= 16) kp.st->round_ns[t] = globaltimer_ns();
-    const uint32_t ch = *(volatile uint32_t*)&kp.st->changed[t];
-    const uint32_t er = *(volatile uint32_t*)&kp.st->err;
+    // one L2 read per CTA, broadcast through shared memory
+    __shared__ uint32_t s_ch, s_er;
+    if (threadIdx.x == 0) {
+      s_ch = *(volatile uint32_t*)&kp.st->changed[t];
+      s_er = *(volatile uint32_t*)&kp.st->err;
+    }
+    __syncthreads();
+    const uint32_t ch = s_ch, er = s_er;
     if ((t >= 2 && ch == 0) || er) {
       if (grid.thread_rank() == 0) kp.st->conv = (t >= 2 && ch == 0) ? t : 0;
       return;
