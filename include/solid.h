@@ -14,10 +14,11 @@
  *     A CUDA failure -> SOLID_ERR_CUDA and the context is poisoned (later calls return
  *     SOLID_ERR_STATE).  solid_last_error() returns a message for the last failure.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is
- *     enqueued on it; solid_lookup_batch blocks the calling thread once per batch to read the
- *     resolver's convergence flags (host-polled resolver).
- *   - Device pointers are caller-owned and must stay valid until the call returns (lookup reads
- *     them until the resolver converged; it synchronises `stream` before returning).
+ *     enqueued on it.  solid_lookup_batch is asynchronous (the resolver loops on the device,
+ *     DESIGN.md §4.4); solid_insert_batch synchronises `stream` once (capacity check, status).
+ *     Batch errors detected on the device (token >= 2^20, user == NONE, bad offsets, request >
+ *     max_blocks) are therefore returned by solid_insert_batch, and nothing is committed.
+ *   - Device pointers are caller-owned and must stay valid until solid_insert_batch returns.
  *   - A context is single-writer (SPEC S:148 single stream); distinct contexts are independent.
  */
 #ifndef SOLID_H

@@ -68,6 +68,7 @@ struct DevStatus {
 };
 
 struct KParams {
+  int policy;
   uint32_t klo[kBS], khi[kBS];     // K_i = B^i split in 32-bit limbs
   unsigned long long ksum_lo, ksum_hi;   // sum_i K_lo, sum_i K_hi (the "+1" of x = token + 1)
   const unsigned long long* mpow;  // M^i, i < max_blocks
@@ -96,6 +97,8 @@ struct KParams {
   uint32_t seg_cap;
   DevStatus* st;
 };
+
+#define POLICY_IS_SOLIDARITY(kp) ((kp).policy == SOLID_POLICY_SOLIDARITY)
 
 __host__ __device__ __forceinline__ uint32_t tag_of(uint32_t epoch, uint32_t sub) {
   return 0xFFFFFFFFu - (epoch * 4096u + sub);
@@ -682,8 +685,12 @@ __global__ void __launch_bounds__(256, 5) k_resolve(KParams kp, uint32_t t_max) 
 // written (a6).  mode 1 commits (optimistically) and counts; mode 2 rolls the batch back exactly:
 // every claimed slot was EMPTY before, so emptying it again restores the previous probe chains.
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_commit(KParams kp, uint32_t tf, int mode) {
+__global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
   constexpr int U = 4;                 // ids per thread, staged so all loads are in flight at once
+  // the converged round is read on the device (lookup never waits for the host); an invalid or
+  // unconverged batch commits nothing
+  if (kp.st->err || (kp.n && kp.st->conv == 0)) return;
+  const uint32_t tf = kp.st->conv == 0 ? 0 : (POLICY_IS_SOLIDARITY(kp) ? kp.st->conv : 0);
   const uint32_t seg = blockIdx.y;
   const uint32_t cnt = min(kp.seg_cnt[seg], kp.seg_cap);
   const int W = (int)(tf & 1);
@@ -869,6 +876,7 @@ struct solid_ctx {
   solid_stats_t stats{};
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint64_t launches = 0;
+  uint64_t resolve_ctas = 0;
   uint32_t seg_host[kNSeg];
   bool ev_valid = false;
 };
@@ -1031,11 +1039,14 @@ static solid_status launch_resolve(solid_ctx* ctx, cudaStream_t s) {
     case SOLID_POLICY_USER_ISOLATION: fn = (const void*)k_resolve<SOLID_POLICY_USER_ISOLATION>; break;
     default: fn = (const void*)k_resolve<SOLID_POLICY_SOLIDARITY>; break;
   }
-  int per_sm = 0, sms = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+  if (!ctx->resolve_ctas) {           // co-resident CTAs (queried once per context)
+    int per_sm = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+    ctx->resolve_ctas = (uint64_t)per_sm * sms;
+  }
   const uint64_t need = (ctx->kp.n * 32 + 255) / 256;
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)per_sm * sms, need));
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ctx->resolve_ctas, need));
   uint32_t tmax = kMaxRounds;
   void* args[] = {(void*)&ctx->kp, (void*)&tmax};
   CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, s));
@@ -1043,7 +1054,7 @@ static solid_status launch_resolve(solid_ctx* ctx, cudaStream_t s) {
 }
 
 static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
-  k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, c->tf, mode);   // 4 staged ids per thread
+  k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, mode);   // 4 staged ids per thread
 }
 
 extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b, solid_result* out,
@@ -1080,6 +1091,7 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   kp.users = b->users;
   kp.enforce = b->enforce;
   kp.n = b->n_requests;
+  kp.policy = ctx->cfg.policy;
   kp.max_blocks = ctx->cfg.max_blocks;
   kp.epoch = ctx->epoch;
   kp.salt = splitmix64(0x5A17ull ^ ((unsigned long long)ctx->epoch << 20));
@@ -1101,7 +1113,6 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t), s));
   CK(cudaEventRecord(ctx->ev[0], s));
   const uint64_t n = b->n_requests;
-  uint32_t rounds = 0;
   ctx->launches = 0;
   if (n) {
     const unsigned grid = grid_for_warps(n);
@@ -1122,30 +1133,7 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
     ctx->launches += 1;
   }
   CK(cudaEventRecord(ctx->ev[5], s));
-  CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (n && !ctx->st_host->err && ctx->st_host->conv == 0)
-    return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
-  if (ctx->cfg.policy == SOLID_POLICY_SOLIDARITY) {
-    ctx->tf = ctx->st_host->conv;
-    rounds = ctx->st_host->conv;
-  } else {
-    ctx->tf = 0;              // APC / USER_ISOLATION commit the round-0 first occurrences
-    rounds = n ? 1 : 0;
-  }
   CK(cudaEventRecord(ctx->ev[2], s));
-  if (ctx->st_host->err) {
-    const uint32_t e = ctx->st_host->err;
-    std::string m = "invalid batch:";
-    if (e & ERR_OFFSETS) m += " offsets";
-    if (e & ERR_TOKEN) m += " token>=2^20";
-    if (e & ERR_USER) m += " user==NONE";
-    if (e & ERR_BLOCKS) m += " request>max_blocks";
-    if (e & ERR_SLOTCAP) m += " tokens>max_batch_tokens";
-    if (e & ERR_SCRATCH) return fail(ctx, SOLID_ERR_CAPACITY, "batch scratch overflow");
-    return fail(ctx, SOLID_ERR_INVALID, m);
-  }
-  ctx->rounds = rounds;
   ctx->pending = true;
   return SOLID_OK;
 }
@@ -1169,6 +1157,20 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   ctx->pending = false;
+  if (ctx->st_host->err) {                 // detected on the device during lookup: nothing committed
+    const uint32_t e = ctx->st_host->err;
+    std::string m = "invalid batch:";
+    if (e & ERR_OFFSETS) m += " offsets";
+    if (e & ERR_TOKEN) m += " token>=2^20";
+    if (e & ERR_USER) m += " user==NONE";
+    if (e & ERR_BLOCKS) m += " request>max_blocks";
+    if (e & ERR_SLOTCAP) m += " tokens>max_batch_tokens";
+    if (e & ERR_SCRATCH) return fail(ctx, SOLID_ERR_CAPACITY, "batch scratch overflow");
+    return fail(ctx, SOLID_ERR_INVALID, m);
+  }
+  if (n && ctx->st_host->conv == 0)
+    return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
+  ctx->rounds = (ctx->cfg.policy == SOLID_POLICY_SOLIDARITY) ? ctx->st_host->conv : (n ? 1u : 0u);
   if (n && ctx->live + ctx->st_host->new_entries > ctx->cfg.capacity_blocks) {
     launch_commit(ctx, 2, s);
     CK(cudaGetLastError());
