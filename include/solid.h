@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SOLID_ABI_VERSION 1u
+#define SOLID_ABI_VERSION 2u
 #define SOLID_USER_NONE 0xFFFFFFFFu   /* "no user": sharer of an unflagged entry */
 
 typedef enum {
@@ -58,6 +58,8 @@ typedef struct {
   uint64_t hash_seed;          /* H-def v2 seed; secret per deployment          */
   int32_t policy;              /* solid_policy                                                   */
   int32_t device;              /* CUDA device ordinal                                            */
+  uint32_t world;              /* shards of the key-hash-partitioned index (1 = single GPU)      */
+  uint32_t rank;               /* this context's shard, < world                                  */
 } solid_config;
 
 typedef struct solid_ctx solid_ctx;
@@ -147,6 +149,37 @@ solid_status solid_checkpoint(solid_ctx* ctx);
 solid_status solid_restore(solid_ctx* ctx);
 
 const char* solid_last_error(const solid_ctx* ctx);
+
+/* ---------------------------------------------------------------------------------------------
+ * Sharded index.  world > 1: each context owns the keys with
+ * owner(key) = ((key >> 32) * world) >> 32 == rank, and admits its own contiguous slice of the
+ * global batch (requests seq_base .. seq_base + n - 1 in global sequence order; slices ordered
+ * by rank).  The caller moves the exchange records between the contexts — all-to-all-v over
+ * NCCL (torch.distributed) across GPUs, or a loopback in one process — in this order:
+ *
+ *   solid_dist_begin                       (hash, local registration; packs REG records)
+ *   exchange REG -> solid_dist_owner_ingest(phase 0)     (owner registration; packs PULL)
+ *   for t = 1, 2, ...:
+ *     exchange PULL -> solid_dist_round(t)   (mirror, Detector round; packs INT records)
+ *     exchange INT  -> solid_dist_owner_ingest(phase t)  (reduce intents; packs PULL)
+ *     changed = max over ranks of solid_dist_round's flag; stop when t >= 2 and !changed
+ *                (APC / USER_ISOLATION: stop after t = 1)
+ *   solid_dist_commit(mode 1); if any rank reports overflow: solid_dist_commit(mode 2)
+ *
+ * Records are 24 bytes.  Send region for peer d starts at record d * cap_records of the send
+ * buffer; receive region for peer s at record s * cap_records of the receive buffer.  Counts
+ * are in records; solid_dist_counts returns the counts of the last pack (per peer).
+ * --------------------------------------------------------------------------------------------- */
+solid_status solid_dist_buffers(solid_ctx* ctx, void** send_dev, void** recv_dev,
+                                uint64_t* cap_records);
+solid_status solid_dist_counts(solid_ctx* ctx, uint64_t* counts_host /* [world] */);
+solid_status solid_dist_begin(solid_ctx* ctx, const solid_batch* local, solid_result* out,
+                              uint64_t seq_base, void* stream);
+solid_status solid_dist_owner_ingest(solid_ctx* ctx, uint32_t phase,
+                                     const uint64_t* recv_counts_host, void* stream);
+solid_status solid_dist_round(solid_ctx* ctx, uint32_t t, const uint64_t* recv_counts_host,
+                              uint32_t* changed, void* stream);
+solid_status solid_dist_commit(solid_ctx* ctx, int mode, uint64_t* new_entries, void* stream);
 
 #ifdef __cplusplus
 }

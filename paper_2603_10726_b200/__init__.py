@@ -28,7 +28,10 @@ ENTRY_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4")])
 # C ABI entry points declared in include/solid.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
                "solid_insert_batch", "solid_admit_host", "solid_stats", "solid_dump",
-               "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error"]
+               "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
+               "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
+               "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit"]
+RECORD_BYTES = 24   # sharded-mode exchange record
 
 
 class SolidError(RuntimeError):
@@ -41,7 +44,8 @@ class _Config(ctypes.Structure):
     _fields_ = [("block_size", ctypes.c_uint32), ("max_blocks", ctypes.c_uint32),
                 ("capacity_blocks", ctypes.c_uint64), ("max_batch_tokens", ctypes.c_uint64),
                 ("max_batch_requests", ctypes.c_uint64), ("hash_seed", ctypes.c_uint64),
-                ("policy", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("policy", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32)]
 
 
 class _Batch(ctypes.Structure):
@@ -98,6 +102,19 @@ def load_library(path: str = LIB_PATH):
         getattr(lib, name).argtypes = [vp]
     lib.solid_last_error.restype = ctypes.c_char_p
     lib.solid_last_error.argtypes = [vp]
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    lib.solid_dist_buffers.restype = st
+    lib.solid_dist_buffers.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), u64p]
+    lib.solid_dist_counts.restype = st
+    lib.solid_dist_counts.argtypes = [vp, u64p]
+    lib.solid_dist_begin.restype = st
+    lib.solid_dist_begin.argtypes = [vp, ctypes.POINTER(_Batch), vp, ctypes.c_uint64, vp]
+    lib.solid_dist_owner_ingest.restype = st
+    lib.solid_dist_owner_ingest.argtypes = [vp, ctypes.c_uint32, u64p, vp]
+    lib.solid_dist_round.restype = st
+    lib.solid_dist_round.argtypes = [vp, ctypes.c_uint32, u64p, ctypes.POINTER(ctypes.c_uint32), vp]
+    lib.solid_dist_commit.restype = st
+    lib.solid_dist_commit.argtypes = [vp, ctypes.c_int, u64p, vp]
     _lib = lib
     return lib
 
@@ -115,10 +132,12 @@ class Index:
 
     def __init__(self, policy: str = "solidarity", capacity_blocks: int = 1 << 20,
                  max_batch_tokens: int = 1 << 24, max_batch_requests: int = 1 << 16,
-                 max_blocks: int = 8192, seed: int = 0x5011D000, device: int = 0):
+                 max_blocks: int = 8192, seed: int = 0x5011D000, device: int = 0,
+                 world: int = 1, rank: int = 0):
         self.lib = load_library()
         cfg = _Config(16, max_blocks, capacity_blocks, max_batch_tokens, max_batch_requests,
-                      seed & 0xFFFFFFFFFFFFFFFF, POLICY[policy], device)
+                      seed & 0xFFFFFFFFFFFFFFFF, POLICY[policy], device, world, rank)
+        self.world, self.rank = world, rank
         h = ctypes.c_void_p()
         rc = self.lib.solid_init(ctypes.byref(cfg), ctypes.byref(h))
         if rc != SOLID_OK:

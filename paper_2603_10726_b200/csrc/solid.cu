@@ -96,6 +96,13 @@ struct KParams {
   uint32_t* seg_cnt;
   uint32_t seg_cap;
   DevStatus* st;
+  // sharded mode: global sequence base of this rank's requests; the local table
+  // holds a mirror of each referenced key's staged state pulled from its owner shard
+  uint64_t seq_base;
+  int dist;
+  unsigned long long* int_ins;     // per local id: this round's earliest local inserter (seq'<<32|user)
+  unsigned long long* int_flg;     // per local id: this round's earliest local flagger
+  uint32_t* mown;                  // per local id: owner user of the mirrored first inserter
 };
 
 #define POLICY_IS_SOLIDARITY(kp) ((kp).policy == SOLID_POLICY_SOLIDARITY)
@@ -191,7 +198,8 @@ __device__ __forceinline__ uint64_t scratch_home(uint64_t key, uint64_t mask) {
 __device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key) {
   uint32_t owner = kNone, sharer = kNone;
   uint64_t ipos = 0;
-  const bool present = index_find(kp, key, owner, sharer, ipos);
+  // sharded mode: a local table entry may belong to another shard; its state comes from there
+  const bool present = !kp.dist && index_find(kp, key, owner, sharer, ipos);
   Cold c;
   c.key = key;
   c.snap_owner = present ? owner : kNone;
@@ -254,6 +262,14 @@ __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool act
           done = true;
         } else {
           const uint32_t mine = seg * kp.seg_cap + idx + 1;
+          if (kp.dist) {      // sharded: a fresh local id has no mirrored state and no intents
+            kp.hot[mine].v[0] = ~0ull;
+            kp.hot[mine].v[1] = ~0ull;
+            kp.int_ins[mine] = ~0ull;
+            kp.int_flg[mine] = ~0ull;
+            kp.mown[mine] = kNone;
+            __threadfence();  // visible before the CAS publishes the id
+          }
           const ulonglong2 nv =
               make_ulonglong2(kx, (unsigned long long)mine | ((unsigned long long)E << 32));
           const ulonglong2 old = atomic_cas128(&kp.stab[pos], e, nv);
@@ -346,7 +362,7 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
                                                           uint32_t seg) {
   const uint64_t sig = (POLICY == SOLID_POLICY_USER_ISOLATION) ? sigma_of(kp.seed, u) : 0;
   const unsigned long long guess =
-      ((unsigned long long)tag_of(kp.epoch, 0) << 32) | (unsigned long long)(j + 1);
+      ((unsigned long long)tag_of(kp.epoch, 0) << 32) | (unsigned long long)(kp.seq_base + j + 1);
   uint64_t carry = 0;
   uint32_t bad = 0;
   BlockWords<SH> cur, nxt;
@@ -434,7 +450,7 @@ __device__ __forceinline__ bool iso_visible(const KParams& kp, uint32_t id, int 
 
 // Evaluates request j in round t; returns true (warp-uniform) if its decision differs from the
 // previous round's (always true in round 1).
-template <int POLICY>
+template <int POLICY, bool DIST>
 __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint64_t j, int lane) {
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
   const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
@@ -448,9 +464,11 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   const uint32_t n = (uint32_t)nb;
   const uint64_t blk0 = o0 >> 4;
   if (n && blk0 + n > kp.slot_cap) return false;
-  const uint32_t seqp = (uint32_t)(j + 1);
-  const int R = (int)((t - 1) & 1), W = (int)(t & 1);
-  const uint32_t tagR = tag_of(kp.epoch, t - 1), tagW = tag_of(kp.epoch, t),
+  const uint32_t seqp = (uint32_t)(kp.seq_base + j + 1);
+  // single GPU: ping-pong by round parity.  Sharded: the pulled mirror always sits in P0 with the
+  // fixed mirror tag (round 1's), and nothing is staged locally (intents go to int_ins/int_flg).
+  const int R = DIST ? 0 : (int)((t - 1) & 1), W = DIST ? 1 : (int)(t & 1);
+  const uint32_t tagR = tag_of(kp.epoch, DIST ? 1 : t - 1), tagW = tag_of(kp.epoch, DIST ? 0 : t),
                  tagS = tag_of(kp.epoch, kSubSnap);
   // speculation: last round's divert depth; its isolated ids are cached in iso_id[]
   const int32_t fprev = (int32_t)prev.y;
@@ -464,7 +482,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   // (snapshot values carry the smallest tag and always pass); likewise "flagged".  Blocks are
   // walked 128 at a time: ids and P[R] pairs of 4 groups of 32 are in flight together.
   const unsigned long long limR = ((unsigned long long)tagR << 32) | seqp;
-  const unsigned long long limW = ((unsigned long long)tagW << 32) | seqp;
+  const unsigned long long limW = DIST ? 0ull : ((unsigned long long)tagW << 32) | seqp;
   uint32_t k = n;
   int32_t f = -1;
   bool carry_flag = false;    // flagged(index g-1) from the previous group
@@ -506,7 +524,8 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
           if (pf && lane <= L && !(g == 0 && lane == 0)) {
             const uint32_t first =
                 ((uint32_t)(pq[q].x >> 32) == tagS) ? 0u : (uint32_t)pq[q].x;
-            const bool pass = vis && owner_from(kp, idq[q], first) == u;
+            const bool pass =
+                vis && (DIST ? kp.mown[idq[q]] : owner_from(kp, idq[q], first)) == u;
             cond = !pass;
           }
           const uint32_t cm = __ballot_sync(0xffffffffu, cond);
@@ -567,7 +586,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
         while (!found && cand) {
           const int L = __ffs(cand) - 1;
           bool present = false;
-          if (lane == L) {
+          if (lane == L && !DIST) {   // sharded: unknown until pulled next round (invisible)
             if (created) {
               present = snap;
             } else {
@@ -594,12 +613,17 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
       const uint32_t id = kp.id_of_block[blk0 + k - 1];
       const Hot* h = kp.hot + id;
       const ulonglong2 p0 = ldw128(&h->v[0]), p1 = ldw128(&h->v[2]);
-      const uint32_t first = gs_first(p0.x, p1.x, R, seqp, tagR, tagW, tagS);
-      const bool flagged = gs_first(p0.y, p1.y, R, seqp, tagR, tagW, tagS) != kNone;
-      if (!flagged && owner_from(kp, id, first) != u) {
+      const uint32_t first = gs_first(p0.x, DIST ? ~0ull : p1.x, R, seqp, tagR, tagW, tagS);
+      const bool flagged =
+          gs_first(p0.y, DIST ? ~0ull : p1.y, R, seqp, tagR, tagW, tagS) != kNone;
+      const uint32_t own = DIST ? kp.mown[id] : owner_from(kp, id, first);
+      if (!flagged && own != u) {
         flagd = k;
-        atomic_min_u64(&kp.hot[id].v[2 * W + 1],
-                       ((unsigned long long)tagW << 32) | (unsigned long long)seqp);
+        if (DIST)
+          atomicMin(&kp.int_flg[id], ((unsigned long long)seqp << 32) | (unsigned long long)u);
+        else
+          atomic_min_u64(&kp.hot[id].v[2 * W + 1],
+                         ((unsigned long long)tagW << 32) | (unsigned long long)seqp);
       }
     }
     flagd = __shfl_sync(0xffffffffu, flagd, 0);
@@ -611,7 +635,12 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
     const uint32_t* ids = (f >= 1) ? kp.iso_id : kp.id_of_block;
     // fire-and-forget RED: within a round, concurrent inserters of one key are rare (a request
     // only inserts keys invisible to it), unlike the hot keys of K_A
-    for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.hot[ids[blk0 + i]].v[2 * W], mine);
+    if (DIST) {
+      const unsigned long long pk = ((unsigned long long)seqp << 32) | (unsigned long long)u;
+      for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.int_ins[ids[blk0 + i]], pk);
+    } else {
+      for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.hot[ids[blk0 + i]].v[2 * W], mine);
+    }
   }
 
   const uint4 d = make_uint4(k, (uint32_t)f, r, flagd);
@@ -649,7 +678,7 @@ __global__ void __launch_bounds__(256, 5) k_resolve(KParams kp, uint32_t t_max) 
     if (threadIdx.x == 0) s_changed = 0;
     __syncthreads();
     bool any = false;
-    for (uint64_t j = w0; j < kp.n; j += nw) any |= eval_request<POLICY>(kp, t, j, lane);
+    for (uint64_t j = w0; j < kp.n; j += nw) any |= eval_request<POLICY, false>(kp, t, j, lane);
     // one store per CTA (100k same-address stores would serialise on one L2 slice)
     if (lane == 0 && any) s_changed = 1;
     __syncthreads();
@@ -877,6 +906,9 @@ struct solid_ctx {
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint64_t launches = 0;
   uint64_t resolve_ctas = 0;
+  // sharded mode (solid_dist.inc)
+  struct Dist* dist = nullptr;
+  uint64_t last_add = 0;
   uint32_t seg_host[kNSeg];
   bool ev_valid = false;
 };
@@ -942,6 +974,9 @@ static solid_status init_scratch(solid_ctx* ctx, cudaStream_t s) {
   return SOLID_OK;
 }
 
+static void dist_free(solid_ctx* ctx);
+static solid_status dist_init(solid_ctx* ctx, uint32_t world, uint32_t rank);
+
 extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   solid_ctx* ctx = nullptr;
   if (!cfg || !out) return SOLID_ERR_INVALID;
@@ -953,8 +988,11 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
     return SOLID_ERR_INVALID;
+  const uint32_t world = cfg->world ? cfg->world : 1;
+  if (world > 64 || cfg->rank >= world) return SOLID_ERR_INVALID;
   ctx = new solid_ctx();
   ctx->cfg = *cfg;
+  ctx->cfg.world = world;
   ctx->dev = cfg->device;
   CK(cudaSetDevice(ctx->dev));
   ctx->tcap = next_pow2(std::max<uint64_t>(2 * cfg->capacity_blocks, 1024));
@@ -1013,6 +1051,15 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   if (rc != SOLID_OK) return rc;
   CK(cudaMemset(ctx->st, 0, sizeof(DevStatus)));
   for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+  if (world > 1) {
+    rc = dist_init(ctx, world, cfg->rank);
+    if (rc != SOLID_OK) {
+      dist_free(ctx);
+      free_all(ctx);
+      delete ctx;
+      return rc;
+    }
+  }
   CK(cudaDeviceSynchronize());
   *out = ctx;
   return SOLID_OK;
@@ -1022,6 +1069,7 @@ extern "C" solid_status solid_destroy(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
+  dist_free(ctx);
   free_all(ctx);
   delete ctx;
   return SOLID_OK;
@@ -1062,6 +1110,7 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   if (!ctx) return SOLID_ERR_INVALID;
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "lookup_batch twice without insert_batch");
+  if (ctx->dist) return fail(ctx, SOLID_ERR_STATE, "sharded context: use the solid_dist_* calls");
   if (!b || (b->n_requests && (!b->tokens || !b->offsets || !b->users || !out)) || !b->offsets)
     return fail(ctx, SOLID_ERR_INVALID, "null batch pointer");
   if (b->n_requests > ctx->cfg.max_batch_requests)
@@ -1092,6 +1141,8 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   kp.enforce = b->enforce;
   kp.n = b->n_requests;
   kp.policy = ctx->cfg.policy;
+  kp.seq_base = 0;
+  kp.dist = 0;
   kp.max_blocks = ctx->cfg.max_blocks;
   kp.epoch = ctx->epoch;
   kp.salt = splitmix64(0x5A17ull ^ ((unsigned long long)ctx->epoch << 20));
@@ -1335,3 +1386,5 @@ extern "C" solid_status solid_restore(solid_ctx* ctx) {
   ctx->live = ctx->live_ckpt;
   return SOLID_OK;
 }
+
+#include "solid_dist.inc"

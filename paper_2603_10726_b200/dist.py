@@ -1,0 +1,205 @@
+"""Sharded index driver: plumbing only.
+
+Every step runs in the C ABI (`solid_dist_*` kernels); this module only moves the exchange
+records between shards and runs the protocol of include/solid.h:
+
+    begin -> [REG] -> owner_ingest(0) -> [PULL] -> { round(t) -> [INT] -> owner_ingest(t)
+          -> allreduce(changed) -> [PULL] } -> commit (-> rollback on any overflow)
+
+Two transports:
+  * `TorchExchange` — one shard per process/GPU; counts by `all_to_all_single`, records by
+    `all_to_all` over the process group (NCCL across GPUs; gloo works for host tensors).
+  * `loopback_admit` — G shards in one process (tests, one GPU): records copied region to region.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import Index, RECORD_BYTES, SOLID_ERR_CAPACITY, SOLID_OK, SolidError, as_numpy
+
+
+class _CudaBuf:
+    """Zero-copy torch view of a device buffer owned by the library."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3}
+
+
+class ShardedIndex:
+    """One shard of the key-hash-partitioned index (one C-ABI context with world > 1)."""
+
+    def __init__(self, world: int, rank: int, policy: str = "solidarity", **kw):
+        import torch
+        self.world, self.rank, self.policy = world, rank, policy
+        self.index = Index(policy, world=world, rank=rank, **kw)
+        lib, h = self.index.lib, self.index.h
+        send, recv, cap = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+        self.index._check(lib.solid_dist_buffers(h, ctypes.byref(send), ctypes.byref(recv),
+                                                 ctypes.byref(cap)))
+        self.cap = int(cap.value)
+        nbytes = world * self.cap * RECORD_BYTES
+        dev = torch.device("cuda", self.index.device)
+        self.send = torch.as_tensor(_CudaBuf(send.value, nbytes), device=dev)
+        self.recv = torch.as_tensor(_CudaBuf(recv.value, nbytes), device=dev)
+        self.out = None
+
+    # ---- regions (byte views) ------------------------------------------------------------
+    def send_region(self, peer: int, records: int):
+        o = peer * self.cap * RECORD_BYTES
+        return self.send[o:o + records * RECORD_BYTES]
+
+    def recv_region(self, peer: int, records: int):
+        o = peer * self.cap * RECORD_BYTES
+        return self.recv[o:o + records * RECORD_BYTES]
+
+    def counts(self) -> np.ndarray:
+        c = (ctypes.c_uint64 * self.world)()
+        self.index._check(self.index.lib.solid_dist_counts(self.index.h, c))
+        return np.array(list(c), dtype=np.int64)
+
+    @staticmethod
+    def _u64arr(v):
+        return (ctypes.c_uint64 * len(v))(*[int(x) for x in v])
+
+    # ---- protocol steps ------------------------------------------------------------------
+    def begin(self, tokens, offsets, users, enforce=None, seq_base: int = 0, stream=None):
+        import torch
+        from . import _Batch
+        n = int(users.numel())
+        self.out = torch.empty((max(n, 1), 6), dtype=torch.int32, device=offsets.device)
+        b = _Batch(n, tokens.data_ptr(), offsets.data_ptr(), users.data_ptr(),
+                   enforce.data_ptr() if enforce is not None else None)
+        self.n = n
+        self.index._check(self.index.lib.solid_dist_begin(
+            self.index.h, ctypes.byref(b), ctypes.c_void_p(self.out.data_ptr()), seq_base,
+            Index._stream(stream)))
+        return self.counts()
+
+    def owner_ingest(self, phase: int, recv_counts, stream=None):
+        self.index._check(self.index.lib.solid_dist_owner_ingest(
+            self.index.h, phase, self._u64arr(recv_counts), Index._stream(stream)))
+        return self.counts()
+
+    def round(self, t: int, recv_counts, stream=None):
+        ch = ctypes.c_uint32()
+        self.index._check(self.index.lib.solid_dist_round(
+            self.index.h, t, self._u64arr(recv_counts), ctypes.byref(ch), Index._stream(stream)))
+        return self.counts(), int(ch.value)
+
+    def commit(self, mode: int, stream=None):
+        add = ctypes.c_uint64()
+        rc = self.index.lib.solid_dist_commit(self.index.h, mode, ctypes.byref(add),
+                                              Index._stream(stream))
+        if rc not in (SOLID_OK, SOLID_ERR_CAPACITY):
+            self.index._check(rc)
+        return rc, int(add.value)
+
+    def results(self):
+        return self.out[:self.n]
+
+
+# ------------------------------------------------------------------------------------------
+# the protocol, shared by both transports
+# ------------------------------------------------------------------------------------------
+def run_protocol(shards_local: Sequence[ShardedIndex], begin_args, exchange, allreduce_max):
+    """Drive the sharded admission for the shards owned by this process.
+
+    exchange(send_counts_per_shard) -> recv_counts_per_shard (moves the records);
+    allreduce_max(list of ints) -> global max.  Returns the per-shard result tensors."""
+    policy = shards_local[0].policy
+    counts = [s.begin(*a) for s, a in zip(shards_local, begin_args)]
+    recv = exchange(counts)                                       # REG
+    counts = [s.owner_ingest(0, rc) for s, rc in zip(shards_local, recv)]
+    recv = exchange(counts)                                       # PULL
+    t = 1
+    while True:
+        outs = [s.round(t, rc) for s, rc in zip(shards_local, recv)]
+        counts = [o[0] for o in outs]
+        changed = allreduce_max([o[1] for o in outs])
+        recv = exchange(counts)                                   # INT
+        counts = [s.owner_ingest(t, rc) for s, rc in zip(shards_local, recv)]
+        if policy != "solidarity" or (t >= 2 and not changed):
+            break
+        recv = exchange(counts)                                   # PULL
+        t += 1
+        if t > 4093:
+            raise SolidError(3, "sharded resolver did not converge")
+    rcs = [s.commit(1)[0] for s in shards_local]
+    if allreduce_max([int(rc == SOLID_ERR_CAPACITY) for rc in rcs]):
+        for s in shards_local:
+            s.commit(2)
+        raise SolidError(SOLID_ERR_CAPACITY, "index shard capacity exceeded; batch rolled back")
+    return [s.results() for s in shards_local], t
+
+
+def loopback_admit(shards: List[ShardedIndex], local_batches, seq_bases):
+    """All shards in this process: REG/PULL/INT records are copied region to region."""
+    import torch
+    G = len(shards)
+
+    def exchange(send_counts):
+        recv_counts = [[int(send_counts[s][r]) for s in range(G)] for r in range(G)]
+        for r in range(G):
+            for s in range(G):
+                k = recv_counts[r][s]
+                if k:
+                    shards[r].recv_region(s, k).copy_(shards[s].send_region(r, k))
+        torch.cuda.synchronize()
+        return recv_counts
+
+    args = [(b["tokens"], b["offsets"], b["users"], b.get("enforce"), sb)
+            for b, sb in zip(local_batches, seq_bases)]
+    return run_protocol(shards, args, exchange, lambda xs: max(xs))
+
+
+class TorchExchange:
+    """One shard per rank of a torch.distributed process group (NCCL for CUDA buffers)."""
+
+    def __init__(self, shard: ShardedIndex, group=None):
+        self.shard, self.group = shard, group
+
+    def exchange(self, send_counts_list):
+        """Counts by all_to_all_single, records by batched point-to-point (NCCL groups them;
+        gloo supports it too, which the CPU tests use)."""
+        import torch
+        import torch.distributed as dist
+        sh = self.shard
+        rank = dist.get_rank(self.group)
+        send_counts = np.asarray(send_counts_list[0], dtype=np.int64)
+        sc = torch.tensor(send_counts, device=sh.send.device)
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = rc.cpu().numpy()
+        ops = []
+        for p in range(sh.world):
+            ns, nr = int(send_counts[p]), int(recv_counts[p])
+            if p == rank:
+                if ns:
+                    sh.recv_region(p, ns).copy_(sh.send_region(p, ns))
+                continue
+            if ns:
+                ops.append(dist.P2POp(dist.isend, sh.send_region(p, ns), p, self.group))
+            if nr:
+                ops.append(dist.P2POp(dist.irecv, sh.recv_region(p, nr), p, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if sh.send.is_cuda:
+            torch.cuda.synchronize()
+        return [recv_counts]
+
+    def allreduce_max(self, xs):
+        import torch
+        import torch.distributed as dist
+        v = torch.tensor([max(xs)], dtype=torch.int64, device=self.shard.send.device)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX, group=self.group)
+        return int(v.item())
+
+    def admit(self, tokens, offsets, users, enforce=None, seq_base: int = 0):
+        res, rounds = run_protocol([self.shard], [(tokens, offsets, users, enforce, seq_base)],
+                                   self.exchange, self.allreduce_max)
+        return res[0], rounds
