@@ -8,10 +8,10 @@ tokens, 80% common system prompt), inputs resident in HBM, on an index restored 
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
 
-N > 1 (torchrun, one process per GPU): every rank admits its own independent tenant partition
-(weak scaling, no data-path collective; the hash-sharded single index is DESIGN.md §7 NEXT); the
-time is the max over ranks.  `--impl reference` times the sequential CPU oracle on the same
-workload (rank 0 only).
+N > 1 (torchrun, one process per GPU): one key-hash-sharded index across the ranks (DESIGN.md
+§7): the global batch is the C2 shape scaled by N, rank r admits its contiguous slice, records
+move over NCCL once per resolver round (timed separately); weak scaling; the time is the max over
+ranks.  `--impl reference` times the sequential CPU oracle on the same workload (rank 0 only).
 """
 from __future__ import annotations
 
@@ -157,6 +157,125 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, world, rank, local):
+    """N > 1: one key-hash-sharded index over all ranks.  The global batch is the
+    C2 shape scaled by N (N x 1000 users sharing the system prompt, N x 100 000 requests, one
+    seeded shuffle); rank r admits its contiguous slice; keys live on their owner shard; the
+    REG / PULL / INT records move over NCCL each resolver round.  Weak scaling: fixed requests
+    per GPU.  Collectives are timed separately (host clock around the exchange calls, after a
+    stream sync; the step itself by CUDA events, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2603_10726_b200 as P
+    from paper_2603_10726_b200.dist import ShardedIndex, TorchExchange, run_protocol
+    from workloads import c2_shared_prompt
+
+    per = 100_000 if args.config == "c2" else 10_000
+    users = (1000 if args.config == "c2" else 100) * world
+    lo, hi = rank * per, (rank + 1) * per
+    s = c2_shared_prompt(users=users, reqs_per_user=100, lo=lo, hi=hi, seed=SEED + 2)
+    nblk = s.n_blocks()
+    dev = torch.device("cuda", local)
+    d = P.to_device(s, dev)
+    shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
+                         max_batch_tokens=s.n_tokens + 64, max_batch_requests=per, seed=SEED,
+                         device=local)
+    ex = TorchExchange(shard)
+    coll = {"s": 0.0}
+
+    def timed_exchange(counts):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = ex.exchange(counts)
+        coll["s"] += time.perf_counter() - t0
+        return r
+
+    def step():
+        res, t = run_protocol([shard], [(d["tokens"], d["offsets"], d["users"], None, lo)],
+                              timed_exchange, ex.allreduce_max)
+        return res[0], t
+
+    for _ in range(max(args.warmup, 1)):
+        shard.index.reset()
+        step()
+    torch.cuda.synchronize()
+    cs = torch.cuda.current_stream(dev)
+    ms, rounds, colls = [], [], []
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            shard.index.reset()
+            dist.barrier()
+            coll["s"] = 0.0
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cs)
+            res, t = step()
+            b.record(cs)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+            rounds.append(t)
+            colls.append(coll["s"] * 1e3)
+        torch.cuda.synchronize()
+        dist.barrier()
+    clocks = clk.summary()
+    tot = torch.tensor([sum(ms), sum(colls)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    tot_ms, coll_ms = float(tot[0]), float(tot[1])
+    value = per * world * args.steps / (tot_ms / 1e3)
+    peak, peak_src = _peaks()
+    alg = (64 * nblk + 37 * per) * world
+    res_np = P.as_numpy(res)
+    # e2e: the same sharded admission from pinned host buffers (H2D + admit + D2H per step)
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(a).pin_memory()
+        ht, ho, hu = pin(s.tokens.view(np.int32)), pin(s.offsets.view(np.int64)), pin(s.users.view(np.int32))
+        et = 0.0
+        for _ in range(args.e2e_steps):
+            shard.index.reset()
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dt, do, du = ht.to(dev, non_blocking=True), ho.to(dev, non_blocking=True), hu.to(dev, non_blocking=True)
+            r, _ = run_protocol([shard], [(dt, do, du, None, lo)], ex.exchange, ex.allreduce_max)
+            r[0].cpu()
+            et += time.perf_counter() - t0
+        tt = torch.tensor([et], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": per * world * args.e2e_steps / float(tt.item()), "unit": "requests/s",
+               "h2d_bytes_per_step": int(ht.numel() * 4 + ho.numel() * 8 + hu.numel() * 4),
+               "d2h_bytes_per_step": int(res_np.nbytes)}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "blocks_per_s": nblk * world * args.steps / (tot_ms / 1e3),
+            "config": {"workload": f"c2_shared_prompt x{world}: {users} users x 100 requests, "
+                                   f"2000-token prompts, {per} requests per GPU",
+                       "policy": "solidarity", "parallelism": f"key-hash-sharded index over "
+                       f"{world} GPUs, NCCL exchange per resolver round",
+                       "l2": "inputs larger than L2", "restore": "index reset before each step"},
+            "roofline": {"bound": "hbm", "kernel": "whole sharded step (per GPU)",
+                         "achieved": alg / world / (tot_ms / args.steps / 1e3) / 1e9,
+                         "peak": peak, "unit": "GB/s",
+                         "frac": alg / world / (tot_ms / args.steps / 1e3) / 1e9 / peak,
+                         "traffic": None, "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": e2e,
+            "gpu_launches": int(sum(6 + 8 * r for r in rounds)),   # begin 2 + ingest0 3 + commit 1; 8 per round
+            "collectives_ms_per_step": coll_ms / args.steps,
+            "resolver_rounds": rounds[-1],
+            "clocks": clocks,
+            "step_ms": ms,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,6 +303,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_sharded(args, world, rank, local)
 
     stream_np, desc = _workload(args.config, rank)
     N = stream_np.n_requests

@@ -102,3 +102,12 @@ def test_c4_small_sharded():
     exp, ed = oracle_run([s.slice(0, 4000), s.slice(4000, s.n_requests)], "solidarity")
     got, gd, _ = sharded_run([s.slice(0, 4000), s.slice(4000, s.n_requests)], 3, "solidarity")
     assert_same(got, exp, gd, ed, "c4 G=3")
+
+
+def test_c2_full_size_sharded_two_shards():
+    """BASELINE configs[1] at full size through the sharded protocol (2 shards, loopback):
+    exactly the sequential answer, like the single-GPU path."""
+    s = c2_shared_prompt()
+    exp, ed = oracle_run([s], "solidarity")
+    got, gd, rounds = sharded_run([s], 2, "solidarity")
+    assert_same(got, exp, gd, ed, "c2full G=2")

@@ -181,29 +181,37 @@ def c1_tiny(seed: int = 0x5011D001) -> Stream:
 # --------------------------------------------------------------------------------------------
 def c2_shared_prompt(users: int = 1000, reqs_per_user: int = 100, sys_tokens: int = 1600,
                      profile_tokens: int = 256, query_tokens: int = 144,
-                     seed: int = 0x5011D002) -> Stream:
+                     seed: int = 0x5011D002, lo: int = 0, hi: int = -1) -> Stream:
     """BASELINE.json configs[1]: every request = common system prompt (1600 tokens = 100 blocks,
     80% of the prompt) + fixed per-user profile (256) + fresh query (144) = 2000 tokens = 125
-    blocks.  Request order is a seeded shuffle of users x reqs_per_user."""
-    n = users * reqs_per_user
+    blocks.  Request order is a seeded shuffle of users x reqs_per_user.  [lo, hi) selects a
+    contiguous slice of that global stream (a rank's share in the sharded benchmark) without
+    materialising the rest."""
+    n_all = users * reqs_per_user
     rng = np.random.default_rng(seed)
     order = np.repeat(np.arange(users, dtype=np.uint32), reqs_per_user)
     rng.shuffle(order)
+    hi = n_all if hi < 0 else hi
+    order = order[lo:hi]
+    n = hi - lo
     L = sys_tokens + profile_tokens + query_tokens
     tok = np.empty((n, L), dtype=np.uint32)
     tok[:, :sys_tokens] = run(seed, K_SYS, 0, sys_tokens)
     if profile_tokens:
-        prof = np.stack([run(seed, K_PROFILE, u, profile_tokens) for u in range(users)])
+        uu = np.unique(order)
+        prof = np.zeros((users, profile_tokens), dtype=np.uint32)
+        for u in uu:
+            prof[int(u)] = run(seed, K_PROFILE, int(u), profile_tokens)
         tok[:, sys_tokens:sys_tokens + profile_tokens] = prof[order]
     if query_tokens:
         base = _key(seed, K_QUERY, 0)
         with np.errstate(over="ignore"):
-            idx = (np.arange(n * query_tokens, dtype=np.uint64) * _GOLD + base)
+            idx = (np.arange(lo * query_tokens, hi * query_tokens, dtype=np.uint64) * _GOLD + base)
         tok[:, sys_tokens + profile_tokens:] = (_splitmix(idx) % np.uint64(VOCAB)).astype(
             np.uint32).reshape(n, query_tokens)
     offsets = np.arange(n + 1, dtype=np.uint64) * np.uint64(L)
     return Stream("c2_shared_prompt", tok.reshape(-1), offsets, order, None,
-                  dict(users=users, reqs_per_user=reqs_per_user, prompt_tokens=L))
+                  dict(users=users, reqs_per_user=reqs_per_user, prompt_tokens=L, lo=lo, hi=hi))
 
 
 # --------------------------------------------------------------------------------------------
