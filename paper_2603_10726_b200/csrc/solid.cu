@@ -464,6 +464,8 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   const uint32_t n = (uint32_t)nb;
   const uint64_t blk0 = o0 >> 4;
   if (n && blk0 + n > kp.slot_cap) return false;
+  const uint32_t* sh_ids = kp.id_of_block + blk0;       // this request's blocks (32-bit indexing)
+  uint32_t* iso_ids = kp.iso_id + blk0;
   const uint32_t seqp = (uint32_t)(kp.seq_base + j + 1);
   // single GPU: ping-pong by round parity.  Sharded: the pulled mirror always sits in P0 with the
   // fixed mirror tag (round 1's), and nothing is staged locally (intents go to int_ins/int_flg).
@@ -474,7 +476,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   const int32_t fprev = (int32_t)prev.y;
   uint32_t iso_pre_id = 0;
   if (POLICY == SOLID_POLICY_SOLIDARITY && fprev >= 1 && (uint32_t)fprev + lane < n)
-    iso_pre_id = kp.iso_id[blk0 + (uint32_t)fprev + lane];
+    iso_pre_id = iso_ids[(uint32_t)fprev + lane];
 
   // ---- a5: first miss k (warp ballot) and barrier scan f over the Shared chain ----
   // During round t, P[R] holds only the snapshot tag, round t-1's tag and older (numerically
@@ -494,7 +496,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t i = base + 32 * q + lane;
-      idq[q] = i < n ? kp.id_of_block[blk0 + i] : 0u;
+      idq[q] = i < n ? sh_ids[i] : 0u;
     }
     if (POLICY == SOLID_POLICY_SOLIDARITY && base == 0 && fprev >= 1 && (uint32_t)fprev + lane < n)
       iso_pre_vis = iso_visible(kp, iso_pre_id, R, limR, limW);
@@ -554,7 +556,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
         const uint32_t i = g + lane;
         bool vis = false;
         if (g == (uint32_t)f) vis = i < n && iso_pre_vis;
-        else if (i < n) vis = iso_visible(kp, kp.iso_id[blk0 + i], R, limR, limW);
+        else if (i < n) vis = iso_visible(kp, iso_ids[i], R, limR, limW);
         const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
         if (inv) {
           m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
@@ -577,7 +579,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
         const uint32_t id = scratch_register(kp, valid, key, seg, lane, created, &snap);
         bool bvis = false;
         if (valid) {
-          kp.iso_id[blk0 + i] = id;
+          iso_ids[i] = id;
           bvis = iso_visible(kp, id, R, limR, limW);
         }
         // lanes not visible through the staged state may still be in the index snapshot; probe
@@ -610,7 +612,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
     // flag rule (R2): e_r = K[k] gets flagged iff owner != u and unflagged; applies with
     // isolation on or off (R11)
     if (lane == 0) {
-      const uint32_t id = kp.id_of_block[blk0 + k - 1];
+      const uint32_t id = sh_ids[k - 1];
       const Hot* h = kp.hot + id;
       const ulonglong2 p0 = ldw128(&h->v[0]), p1 = ldw128(&h->v[2]);
       const uint32_t first = gs_first(p0.x, DIST ? ~0ull : p1.x, R, seqp, tagR, tagW, tagS);
@@ -632,21 +634,21 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   // ---- staged inserts (seq-min scatter); APC / USER_ISOLATION are exact from round 0 ----
   if (POLICY == SOLID_POLICY_SOLIDARITY) {
     const unsigned long long mine = ((unsigned long long)tagW << 32) | (unsigned long long)seqp;
-    const uint32_t* ids = (f >= 1) ? kp.iso_id : kp.id_of_block;
+    const uint32_t* ids = (f >= 1) ? iso_ids : sh_ids;
     // fire-and-forget RED: within a round, concurrent inserters of one key are rare (a request
     // only inserts keys invisible to it), unlike the hot keys of K_A
     if (DIST) {
       const unsigned long long pk = ((unsigned long long)seqp << 32) | (unsigned long long)u;
-      for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.int_ins[ids[blk0 + i]], pk);
+      for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.int_ins[ids[i]], pk);
     } else {
-      for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.hot[ids[blk0 + i]].v[2 * W], mine);
+      for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.hot[ids[i]].v[2 * W], mine);
     }
   }
 
   const uint4 d = make_uint4(k, (uint32_t)f, r, flagd);
   const bool changed =
       t == 1 || prev.x != d.x || prev.y != d.y || prev.z != d.z || prev.w != d.w;
-  if (lane == 0) {
+  if (lane == 0 && changed) {   // an unchanged decision already holds its result
     kp.dec[j] = d;
     const uint32_t kk = (POLICY == SOLID_POLICY_USER_ISOLATION) ? 0u : k;   // no Shared chain
     solid_result res;
@@ -663,11 +665,11 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
 }
 
 // The resolver: all rounds in one persistent cooperative launch (grid = resident CTAs).  Warps
-// stride over the requests; between rounds a grid-wide barrier and a gpu-scope fence (which also
-// invalidates L1, so the next round sees every atomic of this one).  Stops at the first round
+// stride over the requests; between rounds a grid-wide barrier (which also invalidates L1, so the
+// next round sees every atomic of this one).  Stops at the first round
 // t >= 2 whose decisions all equal round t-1's, or after t_max.
 template <int POLICY>
-__global__ void __launch_bounds__(256, 5) k_resolve(KParams kp, uint32_t t_max) {
+__global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) {
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -687,9 +689,9 @@ __global__ void __launch_bounds__(256, 5) k_resolve(KParams kp, uint32_t t_max) 
       if (grid.thread_rank() == 0) kp.st->conv = 1;
       return;
     }
-    __threadfence();
+    // grid.sync(): bar.sync + release/acquire at gpu scope; the acquire path also invalidates
+    // L1 (CCTL.IVALL in SASS), so the next round's weak loads see every write of this one
     grid.sync();
-    __threadfence();
     if (grid.thread_rank() == 0 && t <= 16) kp.st->round_ns[t] = globaltimer_ns();
     // one L2 read per CTA, broadcast through shared memory
     __shared__ uint32_t s_ch, s_er;
