@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark: prefix lookups/s of the CacheSolidarity hot path on B200 (BASELINE.json metric).
 
-A step = one batch admission (solid_lookup_batch + solid_insert_batch: hash, scan, probe, Detector
+A step = one batch admission (solid_admit_batch = lookup + insert: hash, scan, probe, Detector
 resolution, commit) of the C2 workload (BASELINE configs[1]: 1000 users x 100 requests x 2000
 tokens, 80% common system prompt), inputs resident in HBM, on an index restored to the same
 (empty) pre-batch state before every step (restore is outside the timed region).
@@ -317,13 +317,14 @@ def main():
     cs = torch.cuda.current_stream(dev)
 
     def step():
-        idx.lookup(d["tokens"], d["offsets"], d["users"], d["enforce"], out=out)
-        idx.insert()
+        # solid_admit_batch: lookup + commit + device-side capacity check, no host sync inside
+        idx.admit_async(d["tokens"], d["offsets"], d["users"], d["enforce"], out=out)
 
     # warm-up
     for _ in range(args.warmup):
         idx.reset()
         step()
+        idx.status()
     torch.cuda.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -340,6 +341,7 @@ def main():
             ev[k][0].record(cs)
             step()
             ev[k][1].record(cs)
+            idx.status()                # batch status (raises on error), outside the events
             stats = idx.stats()
             for key, f in [("hash", "ms_hash"), ("resolve", "ms_resolve"),
                            ("commit", "ms_commit"), ("hash_kernel", "ms_hash_kernel"),

@@ -130,6 +130,17 @@ solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* batch, solid_
  * for new entries and sharer writes on flagged existing entries.  Checks capacity first. */
 solid_status solid_insert_batch(solid_ctx* ctx, void* stream);
 
+/* Asynchronous lookup + insert (no host synchronisation): the capacity check and the exact
+ * rollback run on the device.  The batch status (SOLID_OK / SOLID_ERR_INVALID /
+ * SOLID_ERR_CAPACITY) is returned by solid_batch_status, which synchronises the stream.  The next
+ * solid_lookup_batch / solid_admit_batch collects it first and returns that earlier batch's
+ * error, if any, without starting the new batch; solid_stats, solid_dump and solid_reset also
+ * collect it.  At most one asynchronous batch is outstanding per context.  A failed batch
+ * leaves the index exactly as before it (device-side exact rollback). */
+solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch, solid_result* out,
+                               void* stream);
+solid_status solid_batch_status(solid_ctx* ctx);
+
 /* lookup + insert with HOST buffers: copies the batch to the device, admits it, copies the
  * results back to out_host (HOST memory) and synchronises `stream`. */
 solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* host_batch,

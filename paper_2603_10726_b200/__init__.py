@@ -28,6 +28,7 @@ ENTRY_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4")])
 # C ABI entry points declared in include/solid.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
                "solid_insert_batch", "solid_admit_host", "solid_stats", "solid_dump",
+               "solid_admit_batch", "solid_batch_status",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
                "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit"]
@@ -91,6 +92,10 @@ def load_library(path: str = LIB_PATH):
     lib.solid_lookup_batch.argtypes = [vp, ctypes.POINTER(_Batch), vp, vp]
     lib.solid_insert_batch.restype = st
     lib.solid_insert_batch.argtypes = [vp, vp]
+    lib.solid_admit_batch.restype = st
+    lib.solid_admit_batch.argtypes = [vp, ctypes.POINTER(_Batch), vp, vp]
+    lib.solid_batch_status.restype = st
+    lib.solid_batch_status.argtypes = [vp]
     lib.solid_admit_host.restype = st
     lib.solid_admit_host.argtypes = [vp, ctypes.POINTER(_Batch), vp, vp]
     lib.solid_stats.restype = st
@@ -195,6 +200,28 @@ class Index:
         out = self.lookup(tokens, offsets, users, enforce, out, stream)
         self.insert(stream)
         return out
+
+    def admit_async(self, tokens, offsets, users, enforce=None, out=None, stream=None):
+        """Lookup + insert without a host synchronisation (solid_admit_batch): the capacity
+        check and exact rollback run on the device.  The batch's status is raised by
+        `status()` (or by the next lookup/admit/stats/dump/reset)."""
+        import torch
+        n = int(users.numel())
+        if out is None:
+            out = torch.empty((max(n, 1), 6), dtype=torch.int32, device=offsets.device)
+        for t in (tokens, offsets, users, out) + ((enforce,) if enforce is not None else ()):
+            if not t.is_cuda or not t.is_contiguous():
+                raise ValueError("batch tensors must be contiguous CUDA tensors")
+        b = _Batch(n, tokens.data_ptr(), offsets.data_ptr(), users.data_ptr(),
+                   enforce.data_ptr() if enforce is not None else None)
+        self._check(self.lib.solid_admit_batch(self.h, ctypes.byref(b),
+                                               ctypes.c_void_p(out.data_ptr()),
+                                               self._stream(stream)))
+        return out[:n]
+
+    def status(self):
+        """Synchronise and raise the outstanding asynchronous batch's error, if any."""
+        self._check(self.lib.solid_batch_status(self.h))
 
     # ---- host-buffer admission (copies inside the C ABI call) -----------------------------
     def admit_host(self, tokens: np.ndarray, offsets: np.ndarray, users: np.ndarray,

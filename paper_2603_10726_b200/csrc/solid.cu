@@ -62,6 +62,8 @@ struct DevStatus {
   uint32_t conv;                         // converged round (0 = not converged)
   unsigned long long new_entries;        // entries claimed by k_commit
   unsigned long long new_flags;          // sharer writes on index (snapshot) entries
+  uint32_t overflow;                     // asynchronous admission: capacity exceeded, rolled back
+  uint32_t pad2;
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t changed[kMaxRounds + 2];
@@ -721,6 +723,10 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
   // the converged round is read on the device (lookup never waits for the host); an invalid or
   // unconverged batch commits nothing
   if (kp.st->err || (kp.n && kp.st->conv == 0)) return;
+  if (mode == 3) {                       // device-decided rollback (asynchronous admission)
+    if (!kp.st->overflow) return;
+    mode = 2;
+  }
   const uint32_t tf = kp.st->conv == 0 ? 0 : (POLICY_IS_SOLIDARITY(kp) ? kp.st->conv : 0);
   const uint32_t seg = blockIdx.y;
   const uint32_t cnt = min(kp.seg_cnt[seg], kp.seg_cap);
@@ -849,6 +855,13 @@ __global__ void __launch_bounds__(256) k_compact(const ulonglong2* tab, uint64_t
   }
 }
 
+// Asynchronous admission: the capacity check on the device (the live count stays resident).
+__global__ void k_capacity_check(DevStatus* st, unsigned long long* live, unsigned long long cap) {
+  if (st->err) return;
+  if (*live + st->new_entries > cap) st->overflow = 1;
+  else *live += st->new_entries;
+}
+
 __global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long v) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -908,6 +921,8 @@ struct solid_ctx {
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint64_t launches = 0;
   uint64_t resolve_ctas = 0;
+  unsigned long long* live_dev = nullptr;   // live count for the asynchronous admission path
+  bool unsynced = false;                    // an asynchronous admission awaits solid_batch_status
   // sharded mode (solid_dist.inc)
   struct Dist* dist = nullptr;
   uint64_t last_add = 0;
@@ -953,6 +968,7 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->dec);
   cudaFree(c->seg_cnt);
   cudaFree(c->st);
+  cudaFree(c->live_dev);
   cudaFree(c->mpow);
   cudaFree(c->gtab);
   cudaFree(c->h_tokens);
@@ -1020,6 +1036,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
             alloc((void**)&ctx->dec, cfg->max_batch_requests * sizeof(uint4)) &&
             alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(uint32_t)) &&
             alloc((void**)&ctx->st, sizeof(DevStatus)) &&
+            alloc((void**)&ctx->live_dev, sizeof(unsigned long long)) &&
             alloc((void**)&ctx->mpow, mb * sizeof(unsigned long long)) &&
             alloc((void**)&ctx->gtab, (mb + 1) * sizeof(unsigned long long)) &&
             cudaMallocHost((void**)&ctx->st_host, sizeof(DevStatus)) == cudaSuccess;
@@ -1052,6 +1069,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   solid_status rc = init_scratch(ctx, 0);
   if (rc != SOLID_OK) return rc;
   CK(cudaMemset(ctx->st, 0, sizeof(DevStatus)));
+  CK(cudaMemset(ctx->live_dev, 0, sizeof(unsigned long long)));
   for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   if (world > 1) {
     rc = dist_init(ctx, world, cfg->rank);
@@ -1112,6 +1130,10 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   if (!ctx) return SOLID_ERR_INVALID;
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "lookup_batch twice without insert_batch");
+  if (ctx->unsynced) {               // collect the outstanding asynchronous batch first
+    solid_status rc = solid_batch_status(ctx);
+    if (rc != SOLID_OK) return rc;
+  }
   if (ctx->dist) return fail(ctx, SOLID_ERR_STATE, "sharded context: use the solid_dist_* calls");
   if (!b || (b->n_requests && (!b->tokens || !b->offsets || !b->users || !out)) || !b->offsets)
     return fail(ctx, SOLID_ERR_INVALID, "null batch pointer");
@@ -1191,12 +1213,9 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   return SOLID_OK;
 }
 
-extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
-  if (!ctx) return SOLID_ERR_INVALID;
-  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
-  if (!ctx->pending) return fail(ctx, SOLID_ERR_STATE, "insert_batch without a pending lookup");
-  cudaStream_t s = (cudaStream_t)stream;
-  CK(cudaSetDevice(ctx->dev));
+// Enqueue the commit of the pending lookup (+ stats and the status copies).  async_mode: the
+// capacity check and the exact rollback also run on the device (no host decision).
+static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mode) {
   const uint64_t n = ctx->kp.n;
   if (n) {
     launch_commit(ctx, 1, s);      // optimistic commit + count; exact rollback on overflow
@@ -1204,12 +1223,22 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
     k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(ctx->kp.out, n, ctx->st);
     CK(cudaGetLastError());
     ctx->launches += 2;
+    if (async_mode) {
+      k_capacity_check<<<1, 1, 0, s>>>(ctx->st, ctx->live_dev, ctx->cfg.capacity_blocks);
+      launch_commit(ctx, 3, s);    // rolls back only if the device saw an overflow
+      CK(cudaGetLastError());
+      ctx->launches += 2;
+    }
   }
   CK(cudaEventRecord(ctx->ev[3], s));
   CK(cudaMemcpyAsync(ctx->seg_host, ctx->seg_cnt, sizeof(ctx->seg_host), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  ctx->pending = false;
+  return SOLID_OK;
+}
+
+// After the stream reached the status copies: report the batch and update the counters.
+static solid_status finish_batch(solid_ctx* ctx, cudaStream_t s, bool async_mode) {
+  const uint64_t n = ctx->kp.n;
   if (ctx->st_host->err) {                 // detected on the device during lookup: nothing committed
     const uint32_t e = ctx->st_host->err;
     std::string m = "invalid batch:";
@@ -1224,7 +1253,10 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   if (n && ctx->st_host->conv == 0)
     return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
   ctx->rounds = (ctx->cfg.policy == SOLID_POLICY_SOLIDARITY) ? ctx->st_host->conv : (n ? 1u : 0u);
-  if (n && ctx->live + ctx->st_host->new_entries > ctx->cfg.capacity_blocks) {
+  if (async_mode) {
+    if (ctx->st_host->overflow)
+      return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9); rolled back");
+  } else if (n && ctx->live + ctx->st_host->new_entries > ctx->cfg.capacity_blocks) {
     launch_commit(ctx, 2, s);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
@@ -1243,6 +1275,9 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   ctx->live += h.new_entries;
   S.live_entries = ctx->live;
   S.last_rounds = ctx->rounds;
+  if (!async_mode)
+    CK(cudaMemcpyAsync(ctx->live_dev, &ctx->live, sizeof(unsigned long long),
+                       cudaMemcpyHostToDevice, s));
   for (int q = 0; q < 8; ++q)
     S.round_us[q] = (q < (int)ctx->rounds && q < 16 && h.round_ns[q + 1] > h.round_ns[0])
                         ? (float)((h.round_ns[q + 1] - h.round_ns[q]) * 1e-3)
@@ -1259,6 +1294,40 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
                         4ull * h.new_flags;
   ctx->ev_valid = true;
   return SOLID_OK;
+}
+
+extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
+  if (!ctx->pending) return fail(ctx, SOLID_ERR_STATE, "insert_batch without a pending lookup");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(ctx->dev));
+  solid_status rc = enqueue_commit(ctx, s, false);
+  if (rc != SOLID_OK) return rc;
+  CK(cudaStreamSynchronize(s));
+  ctx->pending = false;
+  return finish_batch(ctx, s, false);
+}
+
+extern "C" solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch,
+                                          solid_result* out, void* stream) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  solid_status rc = solid_lookup_batch(ctx, batch, out, stream);
+  if (rc != SOLID_OK) return rc;
+  rc = enqueue_commit(ctx, (cudaStream_t)stream, true);
+  if (rc != SOLID_OK) return rc;
+  ctx->pending = false;
+  ctx->unsynced = true;
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_batch_status(solid_ctx* ctx) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  if (!ctx->unsynced) return SOLID_OK;
+  CK(cudaSetDevice(ctx->dev));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->unsynced = false;
+  return finish_batch(ctx, ctx->stream, true);
 }
 
 extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
@@ -1303,6 +1372,7 @@ extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
 
 extern "C" solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out) {
   if (!ctx || !out) return SOLID_ERR_INVALID;
+  if (ctx->unsynced) solid_batch_status(ctx);
   CK(cudaSetDevice(ctx->dev));
   if (ctx->ev_valid) {
     CK(cudaEventSynchronize(ctx->ev[3]));
@@ -1319,6 +1389,7 @@ extern "C" solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out) {
 extern "C" solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64_t cap,
                                    uint64_t* n_out) {
   if (!ctx || !n_out || (cap && !host_out)) return SOLID_ERR_INVALID;
+  if (ctx->unsynced) solid_batch_status(ctx);
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
@@ -1351,6 +1422,7 @@ extern "C" solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64
 
 extern "C" solid_status solid_reset(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
+  if (ctx->unsynced) solid_batch_status(ctx);
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaMemset(ctx->tab, 0, ctx->tcap * sizeof(ulonglong2)));
@@ -1360,7 +1432,9 @@ extern "C" solid_status solid_reset(solid_ctx* ctx) {
   }
   CK(cudaDeviceSynchronize());
   ctx->live = 0;
+  CK(cudaMemset(ctx->live_dev, 0, sizeof(unsigned long long)));
   ctx->pending = false;
+  ctx->unsynced = false;
   ctx->poisoned = false;
   ctx->stats = solid_stats_t{};
   ctx->ev_valid = false;
@@ -1386,6 +1460,7 @@ extern "C" solid_status solid_restore(solid_ctx* ctx) {
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaMemcpy(ctx->tab, ctx->tab_ckpt, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToDevice));
   ctx->live = ctx->live_ckpt;
+  CK(cudaMemcpy(ctx->live_dev, &ctx->live, sizeof(unsigned long long), cudaMemcpyHostToDevice));
   return SOLID_OK;
 }
 

@@ -176,6 +176,47 @@ def test_capacity_overflow_is_all_or_nothing():
     assert (got["reused"] == exp["reused"]).all() and len(idx.dump()) == len(ed)
 
 
+def test_async_admission_matches_and_rolls_back_on_device():
+    """solid_admit_batch: several batches queued with no host sync in between; the results and
+    the index match the oracle; an over-capacity batch is rolled back on the device and reported
+    by solid_batch_status, after which the index keeps admitting."""
+    import torch
+    import paper_2603_10726_b200 as P
+    s = c2_shared_prompt(users=40, reqs_per_user=25)
+    parts = _batches(s, 170)
+    exp, ed = oracle_run(parts, "solidarity")
+    idx = _index("solidarity", parts)
+    outs = []
+    for p in parts:
+        outs.append(idx.admit_async(**P.to_device(p)))
+        torch.cuda.synchronize()   # the results tensor is read below; no host status read yet
+        outs[-1] = P.as_numpy(outs[-1])
+    idx.status()
+    assert_same(np.concatenate(outs), exp, idx.dump(), ed, "async")
+    assert idx.stats()["batches"] == len(parts)
+    # over-capacity batch, then a small one: the first is rolled back on the device
+    r = random_small(60, users=3, alphabet_blocks=50, max_blocks=10, seed=9)
+    idx2 = _index("apc", [r], capacity=r.n_blocks() // 3)
+    idx2.admit_async(**P.to_device(r))
+    with pytest.raises(P.SolidError) as ei:
+        idx2.status()
+    assert ei.value.status == P.SOLID_ERR_CAPACITY
+    assert len(idx2.dump()) == 0 and idx2.stats()["live_entries"] == 0
+    small = r.slice(0, 3)
+    e3, ed3 = oracle_run(small, "apc")
+    got = P.as_numpy(idx2.admit_async(**P.to_device(small)))
+    idx2.status()
+    assert_same(got, e3, idx2.dump(), ed3, "async after rollback")
+    # an error is reported by the next admission when status() was not called
+    idx3 = _index("apc", [r], capacity=r.n_blocks() // 3)
+    idx3.admit_async(**P.to_device(r))
+    with pytest.raises(P.SolidError):
+        idx3.admit_async(**P.to_device(small))
+    idx3.admit_async(**P.to_device(small))
+    idx3.status()
+    assert len(idx3.dump()) == len(ed3)
+
+
 def test_host_buffer_admission_matches():
     s = c1_tiny()
     exp, ed = oracle_run(s, "solidarity")
