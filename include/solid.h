@@ -130,13 +130,21 @@ solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* batch, solid_
  * for new entries and sharer writes on flagged existing entries.  Checks capacity first. */
 solid_status solid_insert_batch(solid_ctx* ctx, void* stream);
 
-/* Asynchronous lookup + insert (no host synchronisation): the capacity check and the exact
- * rollback run on the device.  The batch status (SOLID_OK / SOLID_ERR_INVALID /
- * SOLID_ERR_CAPACITY) is returned by solid_batch_status, which synchronises the stream.  The next
- * solid_lookup_batch / solid_admit_batch collects it first and returns that earlier batch's
- * error, if any, without starting the new batch; solid_stats, solid_dump and solid_reset also
- * collect it.  At most one asynchronous batch is outstanding per context.  A failed batch
- * leaves the index exactly as before it (device-side exact rollback). */
+/* Asynchronous admission (lookup + insert with no host synchronisation), for a pipelined caller.
+ * The capacity check (R9) and the exact rollback of an over-capacity batch run on the device, so
+ * every batch is still all-or-nothing and batches apply in submission order; a failed batch
+ * leaves the index exactly as before it, and later batches see that state.  Up to
+ * SOLID_MAX_INFLIGHT batches may be outstanding; each must be collected, oldest first, by
+ * solid_batch_status, which waits for it and returns ITS status (SOLID_OK, SOLID_ERR_INVALID,
+ * SOLID_ERR_CAPACITY, SOLID_ERR_STATE) and folds it into solid_stats.  With none outstanding
+ * solid_batch_status returns SOLID_OK.  solid_admit_batch itself fails with SOLID_ERR_STATE when
+ * SOLID_MAX_INFLIGHT batches are outstanding or a solid_lookup_batch is pending;
+ * solid_lookup_batch, solid_dump, solid_checkpoint and solid_restore fail with SOLID_ERR_STATE
+ * while any is outstanding.  solid_reset may be called with batches outstanding: it is then
+ * enqueued behind them on their stream without blocking, and the older batches, when
+ * collected, report their status but no longer count in solid_stats.  `out` is written when
+ * the stream reaches the batch (read it after solid_batch_status or a stream synchronisation). */
+#define SOLID_MAX_INFLIGHT 4
 solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch, solid_result* out,
                                void* stream);
 solid_status solid_batch_status(solid_ctx* ctx);
@@ -152,7 +160,8 @@ solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out);
  * number of live entries (may exceed cap; then only cap are written). */
 solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64_t cap, uint64_t* n_out);
 
-/* Empty the index and all scratch (keeps allocations). */
+/* Empty the index (keeps allocations).  Synchronous, unless asynchronous batches are outstanding
+ * (then ordered behind them on their stream, see solid_admit_batch). */
 solid_status solid_reset(solid_ctx* ctx);
 
 /* Save / restore the index contents into / from a ctx-owned device buffer (warm-state reuse). */

@@ -33,6 +33,7 @@ ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
                "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit"]
 RECORD_BYTES = 24   # sharded-mode exchange record
+MAX_INFLIGHT = 4    # SOLID_MAX_INFLIGHT
 
 
 class SolidError(RuntimeError):
@@ -203,8 +204,8 @@ class Index:
 
     def admit_async(self, tokens, offsets, users, enforce=None, out=None, stream=None):
         """Lookup + insert without a host synchronisation (solid_admit_batch): the capacity
-        check and exact rollback run on the device.  The batch's status is raised by
-        `status()` (or by the next lookup/admit/stats/dump/reset)."""
+        check and exact rollback run on the device.  Up to MAX_INFLIGHT batches may be
+        outstanding; `status()` collects the oldest (and raises its error, if any)."""
         import torch
         n = int(users.numel())
         if out is None:
@@ -220,7 +221,7 @@ class Index:
         return out[:n]
 
     def status(self):
-        """Synchronise and raise the outstanding asynchronous batch's error, if any."""
+        """Wait for the oldest outstanding asynchronous batch and raise its error, if any."""
         self._check(self.lib.solid_batch_status(self.h))
 
     # ---- host-buffer admission (copies inside the C ABI call) -----------------------------

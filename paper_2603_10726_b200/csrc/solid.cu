@@ -63,7 +63,8 @@ struct DevStatus {
   unsigned long long new_entries;        // entries claimed by k_commit
   unsigned long long new_flags;          // sharer writes on index (snapshot) entries
   uint32_t overflow;                     // asynchronous admission: capacity exceeded, rolled back
-  uint32_t pad2;
+  uint32_t blocks_done;                  // k_stats last-block detection
+  unsigned long long live_after;         // asynchronous admission: live entries after this batch
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t changed[kMaxRounds + 2];
@@ -808,8 +809,11 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
 }
 
 // Per-batch sums over the results (block-weighted hit rate).
+// With `live` set (asynchronous admission) the last CTA also takes the capacity decision (R9):
+// the live count stays resident on the device and an overflow is flagged for the rollback.
 __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t n,
-                                               DevStatus* st) {
+                                               DevStatus* st, unsigned long long* live,
+                                               unsigned long long cap) {
   unsigned long long a[6] = {0, 0, 0, 0, 0, 0};
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
@@ -831,6 +835,19 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
   }
   __syncthreads();
   if (threadIdx.x < 6 && s_a[threadIdx.x]) atomicAdd(&st->sums[threadIdx.x], s_a[threadIdx.x]);
+  if (!live) return;
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {   // new_entries is final: k_commit completed before us
+    __threadfence();
+    if (!st->err) {
+      const unsigned long long l = *live, add = st->new_entries;
+      if (l + add > cap) st->overflow = 1;
+      else *live = l + add;
+    }
+    st->live_after = *live;
+  }
 }
 
 // Compact the live index slots (dump): warp-aggregated append.
@@ -855,13 +872,6 @@ __global__ void __launch_bounds__(256) k_compact(const ulonglong2* tab, uint64_t
   }
 }
 
-// Asynchronous admission: the capacity check on the device (the live count stays resident).
-__global__ void k_capacity_check(DevStatus* st, unsigned long long* live, unsigned long long cap) {
-  if (st->err) return;
-  if (*live + st->new_entries > cap) st->overflow = 1;
-  else *live += st->new_entries;
-}
-
 __global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long v) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -874,6 +884,16 @@ __global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long
 // Host runtime
 // =============================================================================================
 using namespace solid;
+
+constexpr uint32_t kRing = SOLID_MAX_INFLIGHT;   // asynchronous batches in flight per context
+struct HostSlot {               // pinned host mirror of one batch's status
+  DevStatus st;
+  uint32_t seg[kNSeg];
+};
+struct Flight {                 // one batch in flight: events hash|resolve|commit|done
+  cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  uint64_t n = 0, launches = 0, gen = 0;
+};
 
 struct solid_ctx {
   solid_config cfg{};
@@ -900,7 +920,9 @@ struct solid_ctx {
   uint32_t* seg_cnt = nullptr;
   uint32_t seg_cap = 0;
   DevStatus* st = nullptr;
-  DevStatus* st_host = nullptr;   // pinned mirror
+  DevStatus* st_host = nullptr;   // pinned mirror (the current slot's)
+  uint32_t* seg_host = nullptr;   // pinned per-segment id counts (the current slot's)
+  cudaEvent_t* ev = nullptr;      // the current slot's events
   unsigned long long* mpow = nullptr;
   unsigned long long* gtab = nullptr;
   uint32_t klo[kBS], khi[kBS];
@@ -918,17 +940,26 @@ struct solid_ctx {
   solid_result* h_out = nullptr;
   // stats
   solid_stats_t stats{};
-  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint64_t launches = 0;
   uint64_t resolve_ctas = 0;
   unsigned long long* live_dev = nullptr;   // live count for the asynchronous admission path
-  bool unsynced = false;                    // an asynchronous admission awaits solid_batch_status
+  // batches in flight: a ring of kRing status slots (pinned host mirrors + events); the
+  // asynchronous ones wait in [head, head + outstanding) for solid_batch_status
+  HostSlot* slots = nullptr;
+  Flight fl[kRing];
+  uint32_t head = 0, outstanding = 0, cur = 0;
+  uint64_t gen = 0;                         // reset generation
   // sharded mode (solid_dist.inc)
   struct Dist* dist = nullptr;
   uint64_t last_add = 0;
-  uint32_t seg_host[kNSeg];
-  bool ev_valid = false;
 };
+
+static void set_slot(solid_ctx* c, uint32_t i) {
+  c->cur = i;
+  c->st_host = &c->slots[i].st;
+  c->seg_host = c->slots[i].seg;
+  c->ev = c->fl[i].ev;
+}
 
 static uint64_t next_pow2(uint64_t x) {
   uint64_t p = 1;
@@ -976,9 +1007,10 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->h_users);
   cudaFree(c->h_enforce);
   cudaFree(c->h_out);
-  if (c->st_host) cudaFreeHost(c->st_host);
-  for (auto& e : c->ev)
-    if (e) cudaEventDestroy(e);
+  if (c->slots) cudaFreeHost(c->slots);
+  for (auto& f : c->fl)
+    for (auto& e : f.ev)
+      if (e) cudaEventDestroy(e);
 }
 
 // (Re)initialise the batch scratch: key table stale, staged states at +inf.
@@ -1039,7 +1071,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
             alloc((void**)&ctx->live_dev, sizeof(unsigned long long)) &&
             alloc((void**)&ctx->mpow, mb * sizeof(unsigned long long)) &&
             alloc((void**)&ctx->gtab, (mb + 1) * sizeof(unsigned long long)) &&
-            cudaMallocHost((void**)&ctx->st_host, sizeof(DevStatus)) == cudaSuccess;
+            cudaMallocHost((void**)&ctx->slots, kRing * sizeof(HostSlot)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     free_all(ctx);
@@ -1070,7 +1102,9 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   if (rc != SOLID_OK) return rc;
   CK(cudaMemset(ctx->st, 0, sizeof(DevStatus)));
   CK(cudaMemset(ctx->live_dev, 0, sizeof(unsigned long long)));
-  for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+  for (auto& f : ctx->fl)
+    for (auto& e : f.ev) CK(cudaEventCreate(&e));
+  set_slot(ctx, 0);
   if (world > 1) {
     rc = dist_init(ctx, world, cfg->rank);
     if (rc != SOLID_OK) {
@@ -1125,15 +1159,10 @@ static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
   k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, mode);   // 4 staged ids per thread
 }
 
-extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b, solid_result* out,
-                                           void* stream) {
-  if (!ctx) return SOLID_ERR_INVALID;
+static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result* out,
+                             void* stream) {
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "lookup_batch twice without insert_batch");
-  if (ctx->unsynced) {               // collect the outstanding asynchronous batch first
-    solid_status rc = solid_batch_status(ctx);
-    if (rc != SOLID_OK) return rc;
-  }
   if (ctx->dist) return fail(ctx, SOLID_ERR_STATE, "sharded context: use the solid_dist_* calls");
   if (!b || (b->n_requests && (!b->tokens || !b->offsets || !b->users || !out)) || !b->offsets)
     return fail(ctx, SOLID_ERR_INVALID, "null batch pointer");
@@ -1213,6 +1242,23 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   return SOLID_OK;
 }
 
+static solid_status require_collected(solid_ctx* ctx, const char* what) {
+  if (ctx->outstanding)
+    return fail(ctx, SOLID_ERR_STATE,
+                std::string(what) + " with asynchronous batches outstanding (collect them with "
+                                    "solid_batch_status)");
+  return SOLID_OK;
+}
+
+extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b, solid_result* out,
+                                           void* stream) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  solid_status rc = require_collected(ctx, "lookup_batch");
+  if (rc != SOLID_OK) return rc;
+  if (!ctx->pending) set_slot(ctx, ctx->head);
+  return do_lookup(ctx, b, out, stream);
+}
+
 // Enqueue the commit of the pending lookup (+ stats and the status copies).  async_mode: the
 // capacity check and the exact rollback also run on the device (no host decision).
 static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mode) {
@@ -1220,27 +1266,36 @@ static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mo
   if (n) {
     launch_commit(ctx, 1, s);      // optimistic commit + count; exact rollback on overflow
     CK(cudaGetLastError());
-    k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(ctx->kp.out, n, ctx->st);
+    // asynchronous: k_stats' last CTA also takes the capacity decision on the device
+    k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
+        ctx->kp.out, n, ctx->st, async_mode ? ctx->live_dev : nullptr, ctx->cfg.capacity_blocks);
     CK(cudaGetLastError());
     ctx->launches += 2;
     if (async_mode) {
-      k_capacity_check<<<1, 1, 0, s>>>(ctx->st, ctx->live_dev, ctx->cfg.capacity_blocks);
       launch_commit(ctx, 3, s);    // rolls back only if the device saw an overflow
       CK(cudaGetLastError());
-      ctx->launches += 2;
+      ctx->launches += 1;
     }
   }
   CK(cudaEventRecord(ctx->ev[3], s));
-  CK(cudaMemcpyAsync(ctx->seg_host, ctx->seg_cnt, sizeof(ctx->seg_host), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ctx->seg_host, ctx->seg_cnt, kNSeg * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(ctx->ev[6], s));
+  Flight& f = ctx->fl[ctx->cur];
+  f.n = n;
+  f.launches = ctx->launches;
+  f.gen = ctx->gen;
   return SOLID_OK;
 }
 
-// After the stream reached the status copies: report the batch and update the counters.
-static solid_status finish_batch(solid_ctx* ctx, cudaStream_t s, bool async_mode) {
-  const uint64_t n = ctx->kp.n;
-  if (ctx->st_host->err) {                 // detected on the device during lookup: nothing committed
-    const uint32_t e = ctx->st_host->err;
+// After the stream passed slot i's status copies: report that batch and update the counters.
+// A batch admitted before the last solid_reset only reports its status and per-batch figures.
+static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, bool async_mode) {
+  const Flight& f = ctx->fl[i];
+  const DevStatus& h = ctx->slots[i].st;
+  const uint64_t n = f.n;
+  if (h.err) {                             // detected on the device during lookup: nothing committed
+    const uint32_t e = h.err;
     std::string m = "invalid batch:";
     if (e & ERR_OFFSETS) m += " offsets";
     if (e & ERR_TOKEN) m += " token>=2^20";
@@ -1250,49 +1305,60 @@ static solid_status finish_batch(solid_ctx* ctx, cudaStream_t s, bool async_mode
     if (e & ERR_SCRATCH) return fail(ctx, SOLID_ERR_CAPACITY, "batch scratch overflow");
     return fail(ctx, SOLID_ERR_INVALID, m);
   }
-  if (n && ctx->st_host->conv == 0)
+  if (n && h.conv == 0)
     return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
-  ctx->rounds = (ctx->cfg.policy == SOLID_POLICY_SOLIDARITY) ? ctx->st_host->conv : (n ? 1u : 0u);
+  const bool current = f.gen == ctx->gen;
   if (async_mode) {
-    if (ctx->st_host->overflow)
+    if (h.overflow)
       return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9); rolled back");
-  } else if (n && ctx->live + ctx->st_host->new_entries > ctx->cfg.capacity_blocks) {
+  } else if (n && ctx->live + h.new_entries > ctx->cfg.capacity_blocks) {
     launch_commit(ctx, 2, s);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9)");
   }
-  const DevStatus& h = *ctx->st_host;
   solid_stats_t& S = ctx->stats;
-  S.batches += 1;
-  S.requests += n;
-  S.blocks += h.sums[0];
-  S.reused_blocks += h.sums[1];
-  S.flagged += h.sums[2];
-  S.diverted += h.sums[3];
-  S.truncated += h.sums[4];
-  S.inserted += h.new_entries;
-  ctx->live += h.new_entries;
-  S.live_entries = ctx->live;
+  ctx->rounds = (ctx->cfg.policy == SOLID_POLICY_SOLIDARITY) ? h.conv : (n ? 1u : 0u);
+  if (current) {
+    S.batches += 1;
+    S.requests += n;
+    S.blocks += h.sums[0];
+    S.reused_blocks += h.sums[1];
+    S.flagged += h.sums[2];
+    S.diverted += h.sums[3];
+    S.truncated += h.sums[4];
+    S.inserted += h.new_entries;
+    if (async_mode) {
+      if (n) ctx->live = h.live_after;
+    } else {
+      ctx->live += h.new_entries;
+      CK(cudaMemcpyAsync(ctx->live_dev, &ctx->live, sizeof(unsigned long long),
+                         cudaMemcpyHostToDevice, s));
+    }
+    S.live_entries = ctx->live;
+  }
   S.last_rounds = ctx->rounds;
-  if (!async_mode)
-    CK(cudaMemcpyAsync(ctx->live_dev, &ctx->live, sizeof(unsigned long long),
-                       cudaMemcpyHostToDevice, s));
   for (int q = 0; q < 8; ++q)
     S.round_us[q] = (q < (int)ctx->rounds && q < 16 && h.round_ns[q + 1] > h.round_ns[0])
                         ? (float)((h.round_ns[q + 1] - h.round_ns[q]) * 1e-3)
                         : 0.f;
   uint64_t distinct = 0;
-  for (int q = 0; q < kNSeg; ++q) distinct += std::min<uint32_t>(ctx->seg_host[q], ctx->seg_cap);
+  for (int q = 0; q < kNSeg; ++q)
+    distinct += std::min<uint32_t>(ctx->slots[i].seg[q], ctx->seg_cap);
   S.last_distinct_keys = (uint32_t)std::min<uint64_t>(distinct, 0xFFFFFFFFull);
-  S.last_kernel_launches = ctx->launches;
+  S.last_kernel_launches = f.launches;
   S.last_requests = n;
   S.last_blocks = h.sums[0];
   S.last_inserted = h.new_entries;
   S.last_flagged = h.sums[2];
   S.algorithmic_bytes = 64ull * h.sums[0] + 37ull * n + 16ull * distinct + 16ull * h.new_entries +
                         4ull * h.new_flags;
-  ctx->ev_valid = true;
+  // phase times (the copies behind ev[6] completed, so every event of the batch did)
+  cudaEventElapsedTime(&S.ms_hash, f.ev[0], f.ev[1]);
+  cudaEventElapsedTime(&S.ms_resolve, f.ev[1], f.ev[2]);
+  cudaEventElapsedTime(&S.ms_commit, f.ev[2], f.ev[3]);
+  cudaEventElapsedTime(&S.ms_hash_kernel, f.ev[0], f.ev[1]);
+  cudaEventElapsedTime(&S.ms_round_first, f.ev[4], f.ev[5]);
   return SOLID_OK;
 }
 
@@ -1306,28 +1372,37 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   if (rc != SOLID_OK) return rc;
   CK(cudaStreamSynchronize(s));
   ctx->pending = false;
-  return finish_batch(ctx, s, false);
+  return finish_batch(ctx, ctx->cur, s, false);
 }
 
 extern "C" solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch,
                                           solid_result* out, void* stream) {
   if (!ctx) return SOLID_ERR_INVALID;
-  solid_status rc = solid_lookup_batch(ctx, batch, out, stream);
+  if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "admit_batch with a pending lookup");
+  if (ctx->outstanding == kRing)
+    return fail(ctx, SOLID_ERR_STATE,
+                "SOLID_MAX_INFLIGHT asynchronous batches outstanding (collect one with "
+                "solid_batch_status)");
+  CK(cudaSetDevice(ctx->dev));
+  set_slot(ctx, (ctx->head + ctx->outstanding) % kRing);
+  solid_status rc = do_lookup(ctx, batch, out, stream);
   if (rc != SOLID_OK) return rc;
   rc = enqueue_commit(ctx, (cudaStream_t)stream, true);
-  if (rc != SOLID_OK) return rc;
   ctx->pending = false;
-  ctx->unsynced = true;
+  if (rc != SOLID_OK) return rc;
+  ++ctx->outstanding;
   return SOLID_OK;
 }
 
 extern "C" solid_status solid_batch_status(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
-  if (!ctx->unsynced) return SOLID_OK;
+  if (!ctx->outstanding) return SOLID_OK;
   CK(cudaSetDevice(ctx->dev));
-  CK(cudaStreamSynchronize(ctx->stream));
-  ctx->unsynced = false;
-  return finish_batch(ctx, ctx->stream, true);
+  const uint32_t i = ctx->head;
+  CK(cudaEventSynchronize(ctx->fl[i].ev[6]));
+  ctx->head = (ctx->head + 1) % kRing;
+  --ctx->outstanding;
+  return finish_batch(ctx, i, ctx->stream, true);
 }
 
 extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
@@ -1372,16 +1447,6 @@ extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
 
 extern "C" solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out) {
   if (!ctx || !out) return SOLID_ERR_INVALID;
-  if (ctx->unsynced) solid_batch_status(ctx);
-  CK(cudaSetDevice(ctx->dev));
-  if (ctx->ev_valid) {
-    CK(cudaEventSynchronize(ctx->ev[3]));
-    cudaEventElapsedTime(&ctx->stats.ms_hash, ctx->ev[0], ctx->ev[1]);
-    cudaEventElapsedTime(&ctx->stats.ms_resolve, ctx->ev[1], ctx->ev[2]);
-    cudaEventElapsedTime(&ctx->stats.ms_commit, ctx->ev[2], ctx->ev[3]);
-    cudaEventElapsedTime(&ctx->stats.ms_hash_kernel, ctx->ev[0], ctx->ev[1]);
-    cudaEventElapsedTime(&ctx->stats.ms_round_first, ctx->ev[4], ctx->ev[5]);
-  }
   *out = ctx->stats;
   return SOLID_OK;
 }
@@ -1389,7 +1454,8 @@ extern "C" solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out) {
 extern "C" solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64_t cap,
                                    uint64_t* n_out) {
   if (!ctx || !n_out || (cap && !host_out)) return SOLID_ERR_INVALID;
-  if (ctx->unsynced) solid_batch_status(ctx);
+  solid_status rc0 = require_collected(ctx, "dump");
+  if (rc0 != SOLID_OK) return rc0;
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
@@ -1422,28 +1488,33 @@ extern "C" solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64
 
 extern "C" solid_status solid_reset(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
-  if (ctx->unsynced) solid_batch_status(ctx);
   CK(cudaSetDevice(ctx->dev));
-  if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaMemset(ctx->tab, 0, ctx->tcap * sizeof(ulonglong2)));
+  cudaStream_t s = ctx->stream;
+  if (ctx->poisoned || !ctx->outstanding) {      // synchronous unless batches are in flight
+    if (s) CK(cudaStreamSynchronize(s));
+    CK(cudaDeviceSynchronize());
+  }
+  CK(cudaMemsetAsync(ctx->tab, 0, ctx->tcap * sizeof(ulonglong2), s));
   if (ctx->poisoned) {
-    solid_status rc = init_scratch(ctx, 0);
+    solid_status rc = init_scratch(ctx, s);
     if (rc != SOLID_OK) return rc;
   }
-  CK(cudaDeviceSynchronize());
+  CK(cudaMemsetAsync(ctx->live_dev, 0, sizeof(unsigned long long), s));
+  if (!ctx->outstanding) CK(cudaStreamSynchronize(s));
+  if (ctx->poisoned) ctx->head = ctx->outstanding = 0;   // their results are lost with the state
+  ++ctx->gen;
   ctx->live = 0;
-  CK(cudaMemset(ctx->live_dev, 0, sizeof(unsigned long long)));
   ctx->pending = false;
-  ctx->unsynced = false;
   ctx->poisoned = false;
   ctx->stats = solid_stats_t{};
-  ctx->ev_valid = false;
   return SOLID_OK;
 }
 
 extern "C" solid_status solid_checkpoint(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "checkpoint with a pending batch");
+  solid_status rc0 = require_collected(ctx, "checkpoint");
+  if (rc0 != SOLID_OK) return rc0;
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
   if (!ctx->tab_ckpt) CK(cudaMalloc(&ctx->tab_ckpt, ctx->tcap * sizeof(ulonglong2)));
@@ -1456,6 +1527,8 @@ extern "C" solid_status solid_restore(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
   if (!ctx->tab_ckpt) return fail(ctx, SOLID_ERR_STATE, "restore without checkpoint");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "restore with a pending batch");
+  solid_status rc0 = require_collected(ctx, "restore");
+  if (rc0 != SOLID_OK) return rc0;
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaMemcpy(ctx->tab, ctx->tab_ckpt, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToDevice));

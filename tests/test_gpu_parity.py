@@ -177,44 +177,71 @@ def test_capacity_overflow_is_all_or_nothing():
 
 
 def test_async_admission_matches_and_rolls_back_on_device():
-    """solid_admit_batch: several batches queued with no host sync in between; the results and
-    the index match the oracle; an over-capacity batch is rolled back on the device and reported
-    by solid_batch_status, after which the index keeps admitting."""
+    """solid_admit_batch: up to MAX_INFLIGHT batches queued with no host sync in between, collected
+    oldest first; results and index match the oracle.  An over-capacity batch is rolled back on
+    the device, reported by its own solid_batch_status, and the batches queued behind it see the
+    index without it."""
     import torch
     import paper_2603_10726_b200 as P
     s = c2_shared_prompt(users=40, reqs_per_user=25)
-    parts = _batches(s, 170)
+    parts = _batches(s, 120)
     exp, ed = oracle_run(parts, "solidarity")
     idx = _index("solidarity", parts)
-    outs = []
-    for p in parts:
-        outs.append(idx.admit_async(**P.to_device(p)))
-        torch.cuda.synchronize()   # the results tensor is read below; no host status read yet
-        outs[-1] = P.as_numpy(outs[-1])
-    idx.status()
-    assert_same(np.concatenate(outs), exp, idx.dump(), ed, "async")
-    assert idx.stats()["batches"] == len(parts)
-    # over-capacity batch, then a small one: the first is rolled back on the device
+    dev = [P.to_device(p) for p in parts]
+    outs, inflight = [], 0
+    for d in dev:
+        if inflight == P.MAX_INFLIGHT:
+            with pytest.raises(P.SolidError) as ei:
+                idx.admit_async(**d)
+            assert ei.value.status == P.SOLID_ERR_STATE
+            idx.status()
+            inflight -= 1
+        outs.append(idx.admit_async(**d))
+        inflight += 1
+    with pytest.raises(P.SolidError):
+        idx.dump()                         # outstanding batches must be collected first
+    for _ in range(inflight):
+        idx.status()
+    idx.status()                           # none outstanding: no-op
+    got = np.concatenate([P.as_numpy(o) for o in outs])
+    assert_same(got, exp, idx.dump(), ed, "async")
+    st = idx.stats()
+    assert st["batches"] == len(parts) and st["live_entries"] == len(ed)
+
+    # [small, too-big, small2] queued together: the middle one rolls back on the device
     r = random_small(60, users=3, alphabet_blocks=50, max_blocks=10, seed=9)
+    small, small2 = r.slice(0, 3), r.slice(3, 6)
+    e1, ed1 = oracle_run([small, small2], "apc")
     idx2 = _index("apc", [r], capacity=r.n_blocks() // 3)
+    o1 = idx2.admit_async(**P.to_device(small))
     idx2.admit_async(**P.to_device(r))
+    o3 = idx2.admit_async(**P.to_device(small2))
+    idx2.status()
     with pytest.raises(P.SolidError) as ei:
         idx2.status()
     assert ei.value.status == P.SOLID_ERR_CAPACITY
-    assert len(idx2.dump()) == 0 and idx2.stats()["live_entries"] == 0
-    small = r.slice(0, 3)
-    e3, ed3 = oracle_run(small, "apc")
-    got = P.as_numpy(idx2.admit_async(**P.to_device(small)))
     idx2.status()
-    assert_same(got, e3, idx2.dump(), ed3, "async after rollback")
-    # an error is reported by the next admission when status() was not called
-    idx3 = _index("apc", [r], capacity=r.n_blocks() // 3)
-    idx3.admit_async(**P.to_device(r))
-    with pytest.raises(P.SolidError):
-        idx3.admit_async(**P.to_device(small))
-    idx3.admit_async(**P.to_device(small))
-    idx3.status()
-    assert len(idx3.dump()) == len(ed3)
+    got = np.concatenate([P.as_numpy(o1), P.as_numpy(o3)])
+    assert_same(got, e1, idx2.dump(), ed1, "async rollback in the middle")
+    assert idx2.stats()["live_entries"] == len(ed1)
+
+
+def test_reset_with_batches_in_flight():
+    """solid_reset behind outstanding batches is stream-ordered: the next batch sees an empty
+    index; the older batches still report their status."""
+    import paper_2603_10726_b200 as P
+    s = c1_tiny()
+    exp, ed = oracle_run(s, "solidarity")
+    idx = _index("solidarity", [s])
+    d = P.to_device(s)
+    idx.admit_async(**d)
+    idx.reset()
+    out = idx.admit_async(**d)
+    idx.status()
+    idx.status()
+    assert_same(P.as_numpy(out), exp, idx.dump(), ed, "reset in flight")
+    st = idx.stats()
+    assert st["batches"] == 1 and st["live_entries"] == len(ed)
 
 
 def test_host_buffer_admission_matches():
