@@ -265,7 +265,7 @@ def run_sharded(args, world, rank, local):
                          "traffic": None, "peak_source": peak_src},
             "cpu_baseline": None,
             "e2e": e2e,
-            "gpu_launches": int(sum(6 + 8 * r for r in rounds)),   # begin 2 + ingest0 3 + commit 1; 8 per round
+            "gpu_launches": int(sum(7 + 8 * r for r in rounds)),   # begin 3 + ingest0 3 + commit 1; 8 per round
             "collectives_ms_per_step": coll_ms / args.steps,
             "resolver_rounds": rounds[-1],
             "clocks": clocks,

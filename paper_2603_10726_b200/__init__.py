@@ -13,7 +13,7 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libsolid.so")
+LIB_PATH = os.environ.get("SOLID_LIB") or os.path.join(_PKG, "lib", "libsolid.so")
 
 SOLID_OK, SOLID_ERR_INVALID, SOLID_ERR_CAPACITY, SOLID_ERR_STATE, SOLID_ERR_CUDA, \
     SOLID_ERR_NCCL, SOLID_ERR_OOM = range(7)

@@ -37,6 +37,10 @@ namespace solid {
 namespace cg = cooperative_groups;
 
 constexpr int kNSeg = 128;            // id-allocation segments (spread the allocation atomics)
+struct alignas(128) SegCounter {       // one id counter per 128-byte line: atomics on counters
+  uint32_t v;                          // sharing a line serialise in one L2 slice
+  uint32_t pad[31];
+};
 constexpr uint32_t kSubSnap = 4095;
 constexpr uint32_t kMaxRounds = 4093;
 constexpr uint32_t kMaxEpoch = (0xFFFFFFFFu / 4096u) - 1;
@@ -68,6 +72,10 @@ struct DevStatus {
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t changed[kMaxRounds + 2];
+  uint32_t seg[kNSeg];                   // id counts per segment (gathered by k_stats)
+#ifdef SOLID_COUNTERS
+  unsigned long long cnt[16][8];         // profiling build only: per-round path counters
+#endif
 };
 
 struct KParams {
@@ -96,7 +104,7 @@ struct KParams {
   uint64_t slot_cap;
   uint4* dec;
   solid_result* out;
-  uint32_t* seg_cnt;
+  SegCounter* seg_cnt;
   uint32_t seg_cap;
   DevStatus* st;
   // sharded mode: global sequence base of this rank's requests; the local table
@@ -177,11 +185,10 @@ __device__ __forceinline__ uint32_t gs_first(unsigned long long p0, unsigned lon
 // ---------------------------------------------------------------------------------------------
 // Index probe: linear probing over 16-byte slots {key, owner | sharer << 32}; 0 = empty.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ bool index_find(const KParams& kp, uint64_t key, uint32_t& owner,
-                                           uint32_t& sharer, uint64_t& pos) {
-  pos = key & kp.tmask;
+// Continues a probe whose home slot `e` (at `pos`) was already loaded.
+__device__ __forceinline__ bool index_find_from(const KParams& kp, uint64_t key, ulonglong2 e,
+                                                uint32_t& owner, uint32_t& sharer, uint64_t& pos) {
   for (;;) {
-    const ulonglong2 e = ldw128(&kp.tab[pos]);
     if (e.x == key) {
       owner = (uint32_t)e.y;
       sharer = (uint32_t)(e.y >> 32);
@@ -189,7 +196,14 @@ __device__ __forceinline__ bool index_find(const KParams& kp, uint64_t key, uint
     }
     if (e.x == 0) return false;
     pos = (pos + 1) & kp.tmask;
+    e = ldw128(&kp.tab[pos]);
   }
+}
+
+__device__ __forceinline__ bool index_find(const KParams& kp, uint64_t key, uint32_t& owner,
+                                           uint32_t& sharer, uint64_t& pos) {
+  pos = key & kp.tmask;
+  return index_find_from(kp, key, ldw128(&kp.tab[pos]), owner, sharer, pos);
 }
 
 __device__ __forceinline__ uint64_t scratch_home(uint64_t key, uint64_t mask) {
@@ -198,11 +212,9 @@ __device__ __forceinline__ uint64_t scratch_home(uint64_t key, uint64_t mask) {
 
 // The creator of an id records the key and its index snapshot, and seeds both ping-pong states
 // with it (the snapshot tag is the smallest tag of the batch, so it is never displaced).
-__device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key) {
-  uint32_t owner = kNone, sharer = kNone;
-  uint64_t ipos = 0;
-  // sharded mode: a local table entry may belong to another shard; its state comes from there
-  const bool present = !kp.dist && index_find(kp, key, owner, sharer, ipos);
+__device__ __forceinline__ bool init_id_at(const KParams& kp, uint32_t id, uint64_t key,
+                                           bool present, uint32_t owner, uint32_t sharer,
+                                           uint64_t ipos) {
   Cold c;
   c.key = key;
   c.snap_owner = present ? owner : kNone;
@@ -221,6 +233,14 @@ __device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key) {
     }
   }
   return present;
+}
+
+__device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key) {
+  uint32_t owner = kNone, sharer = kNone;
+  uint64_t ipos = 0;
+  // sharded mode: a local table entry may belong to another shard; its state comes from there
+  const bool present = !kp.dist && index_find(kp, key, owner, sharer, ipos);
+  return init_id_at(kp, id, key, present, owner, sharer, ipos);
 }
 
 // Warp-cooperative find-or-insert of one key per active lane.  Returns the key's id (0 only on
@@ -256,7 +276,7 @@ __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool act
     const uint32_t wm = __ballot_sync(0xffffffffu, want);
     if (wm) {
       uint32_t base = 0;
-      if (lane == __ffs(wm) - 1) base = atomicAdd(&kp.seg_cnt[seg], (uint32_t)__popc(wm));
+      if (lane == __ffs(wm) - 1) base = atomicAdd(&kp.seg_cnt[seg].v, (uint32_t)__popc(wm));
       base = __shfl_sync(0xffffffffu, base, __ffs(wm) - 1);
       if (want) {
         const uint32_t idx = base + __popc(wm & ((1u << lane) - 1u));
@@ -394,7 +414,7 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
 }
 
 template <int POLICY>
-__global__ void __launch_bounds__(256) k_hash_register(KParams kp) {
+__global__ void __launch_bounds__(256, 4) k_hash_register(KParams kp) {
   const int lane = threadIdx.x & 31;
   const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= kp.n) return;
@@ -426,6 +446,18 @@ __global__ void __launch_bounds__(256) k_hash_register(KParams kp) {
     default: bad = hash_register_request<POLICY, 3>(kp, j, lane, base, n, blk0, u, seg); break;
   }
   if (__any_sync(0xffffffffu, bad != 0) && lane == 0) set_err(kp.st, ERR_TOKEN);
+}
+
+// K_A on stream s (single GPU and sharded paths).
+static cudaError_t launch_hash(const KParams& kp, cudaStream_t s) {
+  const unsigned grid = (unsigned)((kp.n * 32 + 255) / 256);
+  switch (kp.policy) {
+    case SOLID_POLICY_APC: k_hash_register<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(kp); break;
+    case SOLID_POLICY_USER_ISOLATION:
+      k_hash_register<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(kp); break;
+    default: k_hash_register<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(kp); break;
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -651,6 +683,19 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   const uint4 d = make_uint4(k, (uint32_t)f, r, flagd);
   const bool changed =
       t == 1 || prev.x != d.x || prev.y != d.y || prev.z != d.z || prev.w != d.w;
+#ifdef SOLID_COUNTERS
+  if (lane == 0 && t < 16) {
+    unsigned long long* c = kp.st->cnt[t];
+    atomicAdd(c + 0, 1ull);
+    if (changed) atomicAdd(c + 1, 1ull);
+    if (f >= 1 && f != fprev) atomicAdd(c + 2, 1ull);
+    if (f >= 1 && f == fprev) atomicAdd(c + 3, 1ull);
+    if (flagd) atomicAdd(c + 4, 1ull);
+    atomicAdd(c + 5, (unsigned long long)(n - r));
+    atomicAdd(c + 6, (unsigned long long)k);
+    if (f >= 1) atomicAdd(c + 7, (unsigned long long)(r - (uint32_t)f));
+  }
+#endif
   if (lane == 0 && changed) {   // an unchanged decision already holds its result
     kp.dec[j] = d;
     const uint32_t kk = (POLICY == SOLID_POLICY_USER_ISOLATION) ? 0u : k;   // no Shared chain
@@ -730,7 +775,7 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
   }
   const uint32_t tf = kp.st->conv == 0 ? 0 : (POLICY_IS_SOLIDARITY(kp) ? kp.st->conv : 0);
   const uint32_t seg = blockIdx.y;
-  const uint32_t cnt = min(kp.seg_cnt[seg], kp.seg_cap);
+  const uint32_t cnt = min(kp.seg_cnt[seg].v, kp.seg_cap);
   const int W = (int)(tf & 1);
   const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
   uint32_t c_new = 0, c_flag = 0;
@@ -813,7 +858,8 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
 // the live count stays resident on the device and an overflow is flagged for the rollback.
 __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t n,
                                                DevStatus* st, unsigned long long* live,
-                                               unsigned long long cap) {
+                                               unsigned long long cap, const SegCounter* seg) {
+  if (blockIdx.x == 0 && threadIdx.x < kNSeg) st->seg[threadIdx.x] = seg[threadIdx.x].v;
   unsigned long long a[6] = {0, 0, 0, 0, 0, 0};
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
@@ -888,7 +934,6 @@ using namespace solid;
 constexpr uint32_t kRing = SOLID_MAX_INFLIGHT;   // asynchronous batches in flight per context
 struct HostSlot {               // pinned host mirror of one batch's status
   DevStatus st;
-  uint32_t seg[kNSeg];
 };
 struct Flight {                 // one batch in flight: events hash|resolve|commit|done
   cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -917,7 +962,7 @@ struct solid_ctx {
   uint32_t* iso_id = nullptr;
   uint64_t slot_cap = 0;
   uint4* dec = nullptr;
-  uint32_t* seg_cnt = nullptr;
+  SegCounter* seg_cnt = nullptr;
   uint32_t seg_cap = 0;
   DevStatus* st = nullptr;
   DevStatus* st_host = nullptr;   // pinned mirror (the current slot's)
@@ -957,7 +1002,7 @@ struct solid_ctx {
 static void set_slot(solid_ctx* c, uint32_t i) {
   c->cur = i;
   c->st_host = &c->slots[i].st;
-  c->seg_host = c->slots[i].seg;
+  c->seg_host = c->slots[i].st.seg;
   c->ev = c->fl[i].ev;
 }
 
@@ -1019,7 +1064,7 @@ static solid_status init_scratch(solid_ctx* ctx, cudaStream_t s) {
   k_fill_u64<<<4096, 256, 0, s>>>(reinterpret_cast<unsigned long long*>(ctx->hot),
                                   ctx->idcap * (sizeof(Hot) / 8), ~0ull);
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
   ctx->epoch = 0;
   return SOLID_OK;
 }
@@ -1066,7 +1111,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
             alloc((void**)&ctx->id_of_block, ctx->slot_cap * sizeof(uint32_t)) &&
             alloc((void**)&ctx->iso_id, ctx->slot_cap * sizeof(uint32_t)) &&
             alloc((void**)&ctx->dec, cfg->max_batch_requests * sizeof(uint4)) &&
-            alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(SegCounter)) &&
             alloc((void**)&ctx->st, sizeof(DevStatus)) &&
             alloc((void**)&ctx->live_dev, sizeof(unsigned long long)) &&
             alloc((void**)&ctx->mpow, mb * sizeof(unsigned long long)) &&
@@ -1214,19 +1259,12 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   kp.seg_cap = ctx->seg_cap;
   kp.st = ctx->st;
   CK(cudaMemsetAsync(ctx->st, 0, sizeof(DevStatus), s));
-  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
   CK(cudaEventRecord(ctx->ev[0], s));
   const uint64_t n = b->n_requests;
   ctx->launches = 0;
   if (n) {
-    const unsigned grid = grid_for_warps(n);
-    switch (ctx->cfg.policy) {
-      case SOLID_POLICY_APC: k_hash_register<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(kp); break;
-      case SOLID_POLICY_USER_ISOLATION:
-        k_hash_register<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(kp); break;
-      default: k_hash_register<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(kp); break;
-    }
-    CK(cudaGetLastError());
+    CK(launch_hash(kp, s));
     ctx->launches = 1;
   }
   CK(cudaEventRecord(ctx->ev[1], s));
@@ -1268,7 +1306,8 @@ static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mo
     CK(cudaGetLastError());
     // asynchronous: k_stats' last CTA also takes the capacity decision on the device
     k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
-        ctx->kp.out, n, ctx->st, async_mode ? ctx->live_dev : nullptr, ctx->cfg.capacity_blocks);
+        ctx->kp.out, n, ctx->st, async_mode ? ctx->live_dev : nullptr, ctx->cfg.capacity_blocks,
+        ctx->seg_cnt);
     CK(cudaGetLastError());
     ctx->launches += 2;
     if (async_mode) {
@@ -1278,7 +1317,6 @@ static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mo
     }
   }
   CK(cudaEventRecord(ctx->ev[3], s));
-  CK(cudaMemcpyAsync(ctx->seg_host, ctx->seg_cnt, kNSeg * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CK(cudaEventRecord(ctx->ev[6], s));
   Flight& f = ctx->fl[ctx->cur];
@@ -1344,7 +1382,7 @@ static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, boo
                         : 0.f;
   uint64_t distinct = 0;
   for (int q = 0; q < kNSeg; ++q)
-    distinct += std::min<uint32_t>(ctx->slots[i].seg[q], ctx->seg_cap);
+    distinct += std::min<uint32_t>(ctx->slots[i].st.seg[q], ctx->seg_cap);
   S.last_distinct_keys = (uint32_t)std::min<uint64_t>(distinct, 0xFFFFFFFFull);
   S.last_kernel_launches = f.launches;
   S.last_requests = n;
@@ -1443,6 +1481,19 @@ extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
   if (n) CK(cudaMemcpyAsync(out_host, ctx->h_out, n * sizeof(solid_result), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return SOLID_OK;
+}
+
+// Profiling build (-DSOLID_COUNTERS) only: the last collected batch's per-round path counters.
+extern "C" solid_status solid_debug_counters(solid_ctx* ctx, unsigned long long* out) {
+#ifdef SOLID_COUNTERS
+  if (!ctx || !out) return SOLID_ERR_INVALID;
+  memcpy(out, ctx->slots[ctx->cur].st.cnt, sizeof(ctx->slots[0].st.cnt));
+  return SOLID_OK;
+#else
+  (void)ctx;
+  (void)out;
+  return SOLID_ERR_STATE;
+#endif
 }
 
 extern "C" solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out) {
