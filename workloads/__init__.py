@@ -5,6 +5,7 @@ ids, request boundaries, user ids and enforce bits.  See ``workloads.gen``.
 """
 from .gen import (Stream, c1_tiny, c2_shared_prompt, c3_multiturn, c4_attackers, random_small,
                   concat_streams, VOCAB)
+from .ttft import TtftStream, query_cuts, ttft_stream
 
 __all__ = ["Stream", "c1_tiny", "c2_shared_prompt", "c3_multiturn", "c4_attackers",
-           "random_small", "concat_streams", "VOCAB"]
+           "random_small", "concat_streams", "VOCAB", "TtftStream", "ttft_stream", "query_cuts"]
