@@ -168,6 +168,45 @@ solid_status solid_reset(solid_ctx* ctx);
 solid_status solid_checkpoint(solid_ctx* ctx);
 solid_status solid_restore(solid_ctx* ctx);
 
+/* ---- Activator -------------------------------------------
+ * per request, selective isolation is enforced iff the hit and miss TTFT distributions
+ * of the most recent sliding window are distinguishable, i.e. their KDE overlap (the integral of
+ * the minimum of the two densities, P:§2.2) is below theta.  Estimator per SPEC S:245-268:
+ * per-token TTFT = ttft_ms / prompt_tokens; Hit if reuse_fraction >= hit_hi, Miss if <= hit_lo,
+ * else excluded; each class keeps its window_len most recent values; Gaussian kernels with
+ * Silverman bandwidth 0.9 min(sd, IQR/1.34) n^-1/5 (sd with ddof 1, linear-interpolation
+ * quartiles, floor 1e-9); trapezoid on `grid` uniform points over [min - 3 h_max, max + 3 h_max];
+ * clamp to [0, 1]; fewer than max(min_samples, 2) values in either class -> enforce (fail-safe).
+ * All arithmetic fp64.  Its enforce[] output is solid_batch.enforce. */
+typedef struct {
+  double theta;            /* overlap threshold in [0, 1]                                  */
+  double hit_hi;           /* reuse fraction >= hit_hi -> Hit sample                       */
+  double hit_lo;           /* reuse fraction <= hit_lo -> Miss sample (hit_lo < hit_hi)    */
+  uint32_t window_len;     /* samples kept per class, 2..4096                              */
+  uint32_t min_samples;    /* per class, below it the decision is "enforce"                */
+  uint32_t grid;           /* trapezoid points, 2..8192 (SPEC: 512)                        */
+  int32_t device;          /* CUDA device ordinal                                          */
+  uint64_t max_samples;    /* capacity of one call's sample stream (< 2^32)                */
+  uint64_t max_queries;    /* capacity of one call's query list                            */
+} solid_activator_config;
+
+typedef struct solid_activator solid_activator;
+
+solid_status solid_activator_init(const solid_activator_config* cfg, solid_activator** out);
+solid_status solid_activator_destroy(solid_activator* act);
+
+/* Device pointers.  ttft_ms[n_samples] (> 0, finite), prompt_tokens[n_samples] (>= 1),
+ * reuse_fraction[n_samples]: the completed requests in completion order.  cuts[n_queries]:
+ * for query j (a request being admitted, sequence order) the number of samples recorded before
+ * it — non-decreasing, <= n_samples.  Writes overlap_out[j] (NaN when fail-safe) and
+ * enforce_out[j] (1 = isolation enforced).  Synchronises `stream` once; invalid samples or cuts
+ * -> SOLID_ERR_INVALID (outputs undefined). */
+solid_status solid_activator_run(solid_activator* act, const double* ttft_ms,
+                                 const uint32_t* prompt_tokens, const double* reuse_fraction,
+                                 uint64_t n_samples, const uint64_t* cuts, uint64_t n_queries,
+                                 double* overlap_out, uint8_t* enforce_out, void* stream);
+const char* solid_activator_last_error(const solid_activator* act);
+
 const char* solid_last_error(const solid_ctx* ctx);
 
 /* ---------------------------------------------------------------------------------------------

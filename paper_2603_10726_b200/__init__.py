@@ -31,7 +31,9 @@ ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup
                "solid_admit_batch", "solid_batch_status",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
-               "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit"]
+               "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit",
+               "solid_activator_init", "solid_activator_destroy", "solid_activator_run",
+               "solid_activator_last_error"]
 RECORD_BYTES = 24   # sharded-mode exchange record
 MAX_INFLIGHT = 4    # SOLID_MAX_INFLIGHT
 
@@ -69,6 +71,14 @@ class _Stats(ctypes.Structure):
                 ("algorithmic_bytes", ctypes.c_uint64),
                 ("last_kernel_launches", ctypes.c_uint64), ("ms_hash_kernel", ctypes.c_float),
                 ("ms_round_first", ctypes.c_float), ("round_us", ctypes.c_float * 8)]
+
+
+class _ActConfig(ctypes.Structure):
+    _fields_ = [("theta", ctypes.c_double), ("hit_hi", ctypes.c_double),
+                ("hit_lo", ctypes.c_double), ("window_len", ctypes.c_uint32),
+                ("min_samples", ctypes.c_uint32), ("grid", ctypes.c_uint32),
+                ("device", ctypes.c_int32), ("max_samples", ctypes.c_uint64),
+                ("max_queries", ctypes.c_uint64)]
 
 
 _lib = None
@@ -121,6 +131,15 @@ def load_library(path: str = LIB_PATH):
     lib.solid_dist_round.argtypes = [vp, ctypes.c_uint32, u64p, ctypes.POINTER(ctypes.c_uint32), vp]
     lib.solid_dist_commit.restype = st
     lib.solid_dist_commit.argtypes = [vp, ctypes.c_int, u64p, vp]
+    lib.solid_activator_init.restype = st
+    lib.solid_activator_init.argtypes = [ctypes.POINTER(_ActConfig), ctypes.POINTER(vp)]
+    lib.solid_activator_destroy.restype = st
+    lib.solid_activator_destroy.argtypes = [vp]
+    lib.solid_activator_run.restype = st
+    lib.solid_activator_run.argtypes = [vp, vp, vp, vp, ctypes.c_uint64, vp, ctypes.c_uint64, vp,
+                                        vp, vp]
+    lib.solid_activator_last_error.restype = ctypes.c_char_p
+    lib.solid_activator_last_error.argtypes = [vp]
     _lib = lib
     return lib
 
@@ -288,3 +307,56 @@ def to_device(stream_obj, device="cuda"):
              enforce=None if stream_obj.enforce is None else
              torch.from_numpy(stream_obj.enforce).to(device))
     return d
+
+
+class Activator:
+    """The Activator (solid_activator_*): per-request enforce bits from the KDE overlap of the
+    hit / miss per-token-TTFT windows (estimator SPEC S:245-268)."""
+
+    def __init__(self, theta: float = 0.5, window_len: int = 256, min_samples: int = 2,
+                 hit_hi: float = 0.8, hit_lo: float = 0.2, grid: int = 512,
+                 max_samples: int = 1 << 20, max_queries: int = 1 << 20, device: int = 0):
+        self.lib = load_library()
+        cfg = _ActConfig(theta, hit_hi, hit_lo, window_len, min_samples, grid, device,
+                         max_samples, max_queries)
+        h = ctypes.c_void_p()
+        rc = self.lib.solid_activator_init(ctypes.byref(cfg), ctypes.byref(h))
+        if rc != SOLID_OK:
+            raise SolidError(rc, "solid_activator_init failed (needs a CUDA device and valid sizes)")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.solid_activator_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, ttft_ms, prompt_tokens, reuse_fraction, cuts, overlap=None, enforce=None,
+            stream=None):
+        """CUDA tensors: ttft_ms float64 [M], prompt_tokens int32/uint32 [M], reuse_fraction
+        float64 [M], cuts int64 [N] (non-decreasing, <= M).  Returns (overlap float64 [N],
+        enforce uint8 [N]); enforce can be passed as a batch's `enforce`."""
+        import torch
+        n, m = int(cuts.numel()), int(ttft_ms.numel())
+        dev = cuts.device
+        if overlap is None:
+            overlap = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        if enforce is None:
+            enforce = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        for t in (ttft_ms, prompt_tokens, reuse_fraction, cuts, overlap, enforce):
+            if not t.is_cuda or not t.is_contiguous():
+                raise ValueError("activator tensors must be contiguous CUDA tensors")
+        st = Index._stream(stream)
+        rc = self.lib.solid_activator_run(self.h, ttft_ms.data_ptr(), prompt_tokens.data_ptr(),
+                                          reuse_fraction.data_ptr(), m, cuts.data_ptr(), n,
+                                          overlap.data_ptr(), enforce.data_ptr(), st)
+        if rc != SOLID_OK:
+            msg = self.lib.solid_activator_last_error(self.h)
+            raise SolidError(rc, msg.decode() if msg else "")
+        return overlap[:n], enforce[:n]

@@ -7,7 +7,7 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SRC = [os.path.join(PKG, "csrc", "solid.cu")]
+SRC = [os.path.join(PKG, "csrc", "solid.cu"), os.path.join(PKG, "csrc", "solid_activator.cu")]
 DEPS = SRC + [os.path.join(PKG, "csrc", "solid_math.cuh"), os.path.join(PKG, "csrc", "solid_dist.inc"),
                os.path.join(ROOT, "include", "solid.h")]
 LIB = os.path.join(PKG, "lib", "libsolid.so")
