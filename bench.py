@@ -123,6 +123,74 @@ def cpu_baseline(stream, sample_requests: int):
                       f"sequential C++ oracle, 1 thread (host has {os.cpu_count()} cores)"}
 
 
+def measure_activator(dev, args):
+    """the Activator over a C2-sized query list — 100 000 queries against a
+    stream of 2^20 completed-request TTFT samples, the window advancing every 100 queries (1 000
+    distinct windows of up to 256 + 256 samples, 512-point grid), inputs resident in HBM."""
+    import torch
+    import paper_2603_10726_b200 as P
+    from workloads import query_cuts, ttft_stream
+    M, N, stride, W, G = 1 << 20, 100_000, 100, 256, 512
+    s = ttft_stream(M, seed=SEED + 0xF2)
+    cuts_np = query_cuts(N, M, stride=stride)
+    d = lambda a, t: torch.from_numpy(np.ascontiguousarray(a)).to(dtype=t, device=dev)
+    tt, pt = d(s.ttft_ms, torch.float64), d(s.prompt_tokens.astype(np.int32), torch.int32)
+    rf, cuts = d(s.reuse_fraction, torch.float64), d(cuts_np, torch.int64)
+    act = P.Activator(theta=0.5, window_len=W, grid=G, max_samples=M, max_queries=N,
+                      device=dev.index or 0)
+    cs = torch.cuda.current_stream(dev)
+    ov, en = act.run(tt, pt, rf, cuts)
+    reps, ms = 5, []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        act.run(tt, pt, rf, cuts, overlap=ov, enforce=en)
+        e1.record(cs)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    med = statistics.median(ms)
+    # work accounting: distinct windows and Gaussian-kernel evaluations (grid x window sizes)
+    hit = np.concatenate([[0], np.cumsum(s.reuse_fraction >= 0.8)])
+    miss = np.concatenate([[0], np.cumsum(s.reuse_fraction <= 0.2)])
+    heads = np.unique(cuts_np)
+    wh, wm = np.minimum(hit[heads], W), np.minimum(miss[heads], W)
+    full = (wh >= 2) & (wm >= 2)
+    evals = int((G * (wh + wm))[full].sum())
+    en_np = en.cpu().numpy()
+    out = {"workload": f"{N} queries, {M} TTFT samples (ttft_stream seed {SEED + 0xF2:#x}), "
+                       f"window every {stride} queries, window_len {W}, grid {G}, theta 0.5",
+           "ms_per_call": med, "ms_all": ms, "queries_per_s": N / (med / 1e3),
+           "windows": int(heads.size), "windows_per_s": heads.size / (med / 1e3),
+           "kernel_evals_per_s": evals / (med / 1e3), "enforced_fraction": float(en_np.mean()),
+           "dtype": "f64", "launches_per_call": 5}
+    # ALU roofline of the window kernel (fp64-bound): fp64 instructions per call from the ncu
+    # capture of this same workload (profiles/latest_ncu.json) over the measured call time,
+    # against the measured DFMA rate (scripts/micro/fp64.cu): instructions, not flops.
+    try:
+        with open(os.path.join(ROOT, "profiles", "latest_ncu.json")) as f:
+            pa = json.load(f)["activator"]
+        inst = pa["k_act_window"]["fp64_warp_instructions"] * 32
+        peak = pa["fp64_peak"]["fma_tflops"] / 2 * 1e12          # DFMA instructions / s
+        out["roofline"] = {"bound": "alu", "kernel": "k_act_window (fp64 KDE)",
+                           "achieved": inst / (med / 1e3) / 1e12, "peak": peak / 1e12,
+                           "unit": "T fp64 instr/s", "frac": inst / (med / 1e3) / peak,
+                           "fp64_pipe_active_pct_ncu": pa["k_act_window"]["fp64_pipe_active_pct"],
+                           "source": "profiles/latest_ncu.json"}
+    except Exception:
+        pass
+    if not args.no_cpu:
+        from oracle.activator import ActivatorConfig, isolation_active, windows
+        cfg = ActivatorConfig(theta=0.5, window_len=W, grid=G)
+        sample = [int(c) for c in np.linspace(2000, 40000, 8).astype(np.int64)]
+        t0 = time.perf_counter()
+        for c in sample:
+            isolation_active(*windows(s.ttft_ms, s.prompt_tokens, s.reuse_fraction, c, cfg), cfg)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": len(sample) / dt, "unit": "windows/s", "cores": 1,
+                               "kind": "oracle", "sample": f"{len(sample)} windows, cuts 2000-40000"}
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -287,6 +355,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=100_000)
     ap.add_argument("--ref-sample", type=int, default=20_000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-activator", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
@@ -425,6 +494,10 @@ def main():
                       "host wall clock (perf_counter) around the call"}
         assert (hout["reused"] == res["reused"]).all()
 
+    activator = None
+    if rank == 0 and world == 1 and not args.profile and not args.no_activator:
+        activator = measure_activator(dev, args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
         cpu = cpu_baseline(stream_np, args.cpu_sample)
@@ -448,6 +521,7 @@ def main():
                                      "step k's status is collected"},
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "activator": activator,
             "e2e": e2e,
             "gpu_launches": int(sum(launches)),
             "clocks": clocks,

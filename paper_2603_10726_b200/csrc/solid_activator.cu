@@ -266,15 +266,16 @@ __global__ void __launch_bounds__(kThreads) k_act_window(Params p) {
   const double step = __ddiv_rn(__dsub_rn(hi, lo), (double)(G - 1));
   const double na = 1.0 / ((double)wh * ha * 2.5066282746310002),   // 1 / (n h sqrt(2 pi))
                nb = 1.0 / ((double)wm * hb * 2.5066282746310002);
+  const double ia = 1.0 / ha, ib = 1.0 / hb;
   for (uint32_t k = threadIdx.x; k < G; k += blockDim.x) {
     const double x = k == G - 1 ? hi : __dadd_rn(__dmul_rn((double)k, step), lo);
     double fa = 0.0, fb = 0.0;
     for (uint32_t i = 0; i < wh; ++i) {
-      const double d = __ddiv_rn(__dsub_rn(x, A[i]), ha);
+      const double d = __dsub_rn(x, A[i]) * ia;
       fa += exp(-0.5 * d * d);
     }
     for (uint32_t i = 0; i < wm; ++i) {
-      const double d = __ddiv_rn(__dsub_rn(x, B[i]), hb);
+      const double d = __dsub_rn(x, B[i]) * ib;
       fb += exp(-0.5 * d * d);
     }
     M[k] = fmin(fa * na, fb * nb);
