@@ -21,6 +21,8 @@ POLICY_APC, POLICY_USER_ISOLATION, POLICY_SOLIDARITY = 0, 1, 2
 RESULT_DTYPE = np.dtype([("n_blocks", "<u4"), ("shared_hits", "<u4"), ("reused", "<u4"),
                          ("divert_at", "<i4"), ("flag_depth", "<u4"), ("bits", "<u4")])
 ENTRY_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4")])
+ENTRY_EX_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4"),
+                           ("last_used", "<u8")])
 
 
 def build_oracle(force: bool = False) -> str:
@@ -60,6 +62,14 @@ def _load():
         lib.oracle_dump.argtypes = [vp, vp, u64]
         lib.oracle_copy_table.argtypes = [vp, vp]
         lib.oracle_reserve.argtypes = [vp, u64]
+        lib.oracle_set_capacity.restype = ctypes.c_int
+        lib.oracle_set_capacity.argtypes = [vp, u64]
+        lib.oracle_evictions.restype = u64
+        lib.oracle_evictions.argtypes = [vp]
+        lib.oracle_next_seq.restype = u64
+        lib.oracle_next_seq.argtypes = [vp]
+        lib.oracle_dump_ex.restype = u64
+        lib.oracle_dump_ex.argtypes = [vp, vp, u64]
         _lib = lib
     return _lib
 
@@ -71,12 +81,16 @@ def _ptr(a: Optional[np.ndarray]):
 class Oracle:
     """Sequential reference: Oracle(block_size, seed, policy).process(stream) -> results."""
 
-    def __init__(self, block_size: int = 16, seed: int = 0, policy: int = POLICY_SOLIDARITY):
+    def __init__(self, block_size: int = 16, seed: int = 0, policy: int = POLICY_SOLIDARITY,
+                 capacity: int = 0):
         self.lib = _load()
         self.block_size, self.seed, self.policy = block_size, seed, policy
         self.h = self.lib.oracle_create(block_size, seed & 0xFFFFFFFFFFFFFFFF, policy)
         if not self.h:
             raise ValueError("oracle_create: bad arguments")
+        self.capacity = capacity
+        if capacity:
+            self.lib.oracle_set_capacity(self.h, capacity)   # LRU eviction (DESIGN.md R22-R25)
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -120,6 +134,19 @@ class Oracle:
         out = np.zeros(max(n, 1), dtype=ENTRY_DTYPE)
         self.lib.oracle_dump(self.h, _ptr(out), n)
         return out[:n]
+
+    def dump_ex(self) -> np.ndarray:
+        """Live entries with their LRU clock (last_used), sorted by key."""
+        n = self.size()
+        out = np.zeros(max(n, 1), dtype=ENTRY_EX_DTYPE)
+        self.lib.oracle_dump_ex(self.h, _ptr(out), n)
+        return out[:n]
+
+    def evictions(self) -> int:
+        return int(self.lib.oracle_evictions(self.h))
+
+    def next_seq(self) -> int:
+        return int(self.lib.oracle_next_seq(self.h))
 
     def params(self):
         B, M = ctypes.c_uint64(), ctypes.c_uint64()

@@ -23,7 +23,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <set>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 namespace {
@@ -63,8 +65,10 @@ uint64_t key_of(uint64_t S) {
 }
 
 struct Entry {
-  uint32_t owner;    // OwnerID: set exactly once at allocation
-  uint32_t sharer;   // user that flagged the entry; AttackFlag <=> sharer != NONE (R5)
+  uint32_t owner;     // OwnerID: set exactly once at allocation
+  uint32_t sharer;    // user that flagged the entry; AttackFlag <=> sharer != NONE (R5)
+  uint64_t last_used; // LRU clock (R22): global sequence number of the last request
+                      // that was served this entry or inserted it
 };
 
 struct Ctx {
@@ -75,6 +79,12 @@ struct Ctx {
   std::vector<uint64_t> K;   // K_i = B^i mod p
   std::unordered_map<uint64_t, Entry> table;
   uint64_t next_seq;
+  // LRU eviction (SPEC evict_lru S:117-125; R22-R25).  capacity 0 = unbounded (no
+  // eviction, R9).  lru orders the live entries by (last_used, key): the first element is the
+  // victim ("smallest last_used; ties broken by smaller hash value").
+  uint64_t capacity;
+  std::set<std::pair<uint64_t, uint64_t>> lru;
+  uint64_t evictions;
 };
 
 uint64_t sigma_of(const Ctx& c, uint32_t user) {
@@ -99,10 +109,37 @@ bool present(const Ctx& c, uint64_t key) { return c.table.count(key) != 0; }
 bool flagged(const Ctx& c, uint64_t key) { return c.table.at(key).sharer != NONE; }
 uint32_t owner_of(const Ctx& c, uint64_t key) { return c.table.at(key).owner; }
 
-// "On a cache miss, a new cache entry is created and tagged with the user's ID".
-// Inserting a key that is already present leaves it unchanged (R8).
-void insert_if_absent(Ctx& c, uint64_t key, uint32_t user) {
-  if (!present(c, key)) c.table.emplace(key, Entry{user, (uint32_t)NONE});
+// "On a cache miss, a new cache entry is created and tagged with the user's ID",
+// with last_used = the request's clock.  Inserting a key that is already present leaves
+// it unchanged — owner, flag and last_used (R8, R23).
+void insert_if_absent(Ctx& c, uint64_t key, uint32_t user, uint64_t seq) {
+  if (present(c, key)) return;
+  c.table.emplace(key, Entry{user, (uint32_t)NONE, seq});
+  if (c.capacity) c.lru.insert(std::make_pair(seq, key));
+}
+
+// An entry whose cached content is served to the request refreshes its last_used (R23).
+void touch(Ctx& c, uint64_t key, uint64_t seq) {
+  Entry& e = c.table.at(key);
+  if (c.capacity) {
+    c.lru.erase(std::make_pair(e.last_used, key));
+    c.lru.insert(std::make_pair(seq, key));
+  }
+  e.last_used = seq;
+}
+
+// evict_lru: while the table holds more than `capacity` entries, remove the entry
+// with the smallest last_used, ties broken by the smaller key; its owner and flag die with it
+// (S:120).  Applied after the request's inserts ("if capacity exceeded, evict_lru is
+// applied until the invariant holds"; R24).
+void evict_to_capacity(Ctx& c) {
+  if (!c.capacity) return;
+  while (c.table.size() > c.capacity) {
+    auto victim = c.lru.begin();
+    c.table.erase(victim->second);
+    c.lru.erase(victim);
+    ++c.evictions;
+  }
 }
 
 }  // namespace
@@ -137,8 +174,21 @@ void* oracle_create(uint32_t block_size, uint64_t seed, int policy) {
   for (uint32_t i = 0; i < block_size; ++i) { c->K[i] = pw; pw = mulmod(pw, c->B); }
   c->M = pw;                  // M = B^bs
   c->next_seq = 0;
+  c->capacity = 0;
+  c->evictions = 0;
   return c;
 }
+
+// LRU capacity in entries (0 = unbounded).  Must be set on an empty table.
+int oracle_set_capacity(void* h, uint64_t capacity) {
+  Ctx* c = (Ctx*)h;
+  if (!c->table.empty()) return 1;
+  c->capacity = capacity;
+  return 0;
+}
+
+uint64_t oracle_evictions(void* h) { return ((Ctx*)h)->evictions; }
+uint64_t oracle_next_seq(void* h) { return ((Ctx*)h)->next_seq; }
 
 void oracle_destroy(void* h) { delete (Ctx*)h; }
 
@@ -217,7 +267,8 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
         I[b] = key_of(T);
       }
       while (r < n && present(c, I[r + 1])) ++r;
-      for (uint32_t b = r + 1; b <= n; ++b) insert_if_absent(c, I[b], u);
+      for (uint32_t b = 1; b <= r; ++b) touch(c, I[b], c.next_seq);
+      for (uint32_t b = r + 1; b <= n; ++b) insert_if_absent(c, I[b], u, c.next_seq);
       f = 0;
     } else {
       // Shared chain S[b] and keys K[b]
@@ -236,7 +287,8 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
       if (c.policy == 0) {
         // Prefix Caching baseline: full reuse, new entries tagged with owner, no flags.
         r = k;
-        for (uint32_t b = k + 1; b <= n; ++b) insert_if_absent(c, Kk[b], u);
+        for (uint32_t b = 1; b <= k; ++b) touch(c, Kk[b], c.next_seq);
+        for (uint32_t b = k + 1; b <= n; ++b) insert_if_absent(c, Kk[b], u, c.next_seq);
       } else {
         // Detector.  Enforcement scan, only while isolation is active:
         // a hit on a flagged prefix continues only if the NEXT prefix belongs to the requester
@@ -258,7 +310,9 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
             c.table.at(Kk[k]).sharer = u;
             flagd = k;
           }
-          for (uint32_t b = k + 1; b <= n; ++b) insert_if_absent(c, Kk[b], u);
+          // the served chain K[1..k] (incl. the entry just flagged) refreshes (R23)
+          for (uint32_t b = 1; b <= k; ++b) touch(c, Kk[b], c.next_seq);
+          for (uint32_t b = k + 1; b <= n; ++b) insert_if_absent(c, Kk[b], u, c.next_seq);
         } else {
           // Selective isolation: reuse stops at the flagged prefix f; the
           // remaining blocks continue in the requester's isolated namespace rooted at S[f]
@@ -276,10 +330,15 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
           uint32_t m = 0;
           while ((uint32_t)f + m < n && present(c, I[(uint32_t)f + m + 1])) ++m;
           r = (uint32_t)f + m;
-          for (uint32_t b = r + 1; b <= n; ++b) insert_if_absent(c, I[b], u);
+          // served: Shared K[1..f] (the flagged entry included; SPEC S:157 open question) and
+          // Iso I[f+1..r].  Truncated Shared entries K[f+1..k] are not served (R23).
+          for (uint32_t b = 1; b <= (uint32_t)f; ++b) touch(c, Kk[b], c.next_seq);
+          for (uint32_t b = (uint32_t)f + 1; b <= r; ++b) touch(c, I[b], c.next_seq);
+          for (uint32_t b = r + 1; b <= n; ++b) insert_if_absent(c, I[b], u, c.next_seq);
         }
       }
     }
+    evict_to_capacity(c);
     oracle_result& o = out[j];
     o.n_blocks = n;
     o.shared_hits = (c.policy == 1) ? 0 : k;
@@ -305,8 +364,37 @@ uint64_t oracle_dump(void* h, oracle_entry* out, uint64_t cap) {
   return v.size();
 }
 
-// Copy the table state of one ctx into another (warm-state reuse in tests / bench).
-void oracle_copy_table(void* dst, void* src) { ((Ctx*)dst)->table = ((Ctx*)src)->table; }
+struct oracle_entry_ex {
+  uint64_t key;
+  uint32_t owner;
+  uint32_t sharer;
+  uint64_t last_used;
+};
+
+// Table dump with the LRU clock, sorted by key.
+uint64_t oracle_dump_ex(void* h, oracle_entry_ex* out, uint64_t cap) {
+  Ctx& c = *(Ctx*)h;
+  std::vector<oracle_entry_ex> v;
+  v.reserve(c.table.size());
+  for (auto& kv : c.table)
+    v.push_back(oracle_entry_ex{kv.first, kv.second.owner, kv.second.sharer, kv.second.last_used});
+  std::sort(v.begin(), v.end(),
+            [](const oracle_entry_ex& a, const oracle_entry_ex& b) { return a.key < b.key; });
+  uint64_t n = std::min<uint64_t>(cap, v.size());
+  if (n) std::memcpy(out, v.data(), n * sizeof(oracle_entry_ex));
+  return v.size();
+}
+
+// Copy the table state (and clock, LRU order) of one ctx into another (warm-state reuse).
+void oracle_copy_table(void* dst, void* src) {
+  Ctx* d = (Ctx*)dst;
+  const Ctx* s = (const Ctx*)src;
+  d->table = s->table;
+  d->lru = s->lru;
+  d->capacity = s->capacity;
+  d->evictions = s->evictions;
+  d->next_seq = s->next_seq;
+}
 
 void oracle_reserve(void* h, uint64_t n) { ((Ctx*)h)->table.reserve(n); }
 

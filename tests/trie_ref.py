@@ -14,10 +14,37 @@ NONE = 0xFFFFFFFF
 
 
 class TrieRef:
-    def __init__(self, block_size: int = 16, policy: int = 2):
+    """capacity > 0 adds LRU eviction (SPEC evict_lru S:117-125, R22-R25), brute force:
+    every entry carries last_used = the clock of the last request served it or that inserted it;
+    after a request's inserts, while more than `capacity` entries are live, the one with the
+    smallest (last_used, key) is removed by a linear scan.  `keyfn(name)` gives the entry's hash
+    value, needed only for the tie-break ("ties broken by smaller hash value")."""
+
+    def __init__(self, block_size: int = 16, policy: int = 2, capacity: int = 0, keyfn=None):
         self.bs = block_size
         self.policy = policy
         self.table = {}     # name -> [owner, sharer]
+        self.capacity = capacity
+        self.keyfn = keyfn
+        self.last_used = {}  # name -> clock
+        self.clock = 0
+        self.evictions = 0
+
+    def _served(self, names):
+        for nm in names:
+            self.last_used[nm] = self.clock
+
+    def _insert(self, t, name, u):
+        if name not in t:
+            t[name] = [u, NONE]
+            self.last_used[name] = self.clock
+
+    def _evict(self):
+        while self.capacity and len(self.table) > self.capacity:
+            victim = min(self.table, key=lambda nm: (self.last_used[nm], self.keyfn(nm)))
+            del self.table[victim]
+            del self.last_used[victim]
+            self.evictions += 1
 
     def _blocks(self, toks):
         n = len(toks) // self.bs
@@ -33,8 +60,9 @@ class TrieRef:
             names = [("I", (), u, tuple(blk[:b])) for b in range(1, n + 1)]
             while r < n and names[r] in t:
                 r += 1
+            self._served(names[:r])
             for b in range(r, n):
-                t.setdefault(names[b], [u, NONE])
+                self._insert(t, names[b], u)
             f = 0
         else:
             shared = [("S", tuple(blk[:b])) for b in range(1, n + 1)]
@@ -42,8 +70,9 @@ class TrieRef:
                 k += 1
             if self.policy == 0:
                 r = k
+                self._served(shared[:k])
                 for b in range(k, n):
-                    t.setdefault(shared[b], [u, NONE])
+                    self._insert(t, shared[b], u)
             else:
                 if e:
                     for b in range(1, k + 1):
@@ -59,8 +88,9 @@ class TrieRef:
                         if ent[0] != u and ent[1] == NONE:
                             ent[1] = u
                             flagd = k
+                    self._served(shared[:k])
                     for b in range(k, n):
-                        t.setdefault(shared[b], [u, NONE])
+                        self._insert(t, shared[b], u)
                 else:
                     root = tuple(blk[:f])
                     iso = [("I", root, u, tuple(blk[f:b])) for b in range(f + 1, n + 1)]
@@ -68,8 +98,11 @@ class TrieRef:
                     while m < len(iso) and iso[m] in t:
                         m += 1
                     r = f + m
+                    self._served(shared[:f] + iso[:m])
                     for name in iso[m:]:
-                        t.setdefault(name, [u, NONE])
+                        self._insert(t, name, u)
+        self._evict()
+        self.clock += 1
         bits = ((1 if r > 0 else 0) | (2 if (n > 0 and r == n) else 0) | (4 if f >= 0 else 0)
                 | (8 if (f >= 0 and f < k) else 0) | (16 if flagd > 0 else 0))
         return (n, 0 if self.policy == 1 else k, r, f, flagd, bits)
