@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SOLID_ABI_VERSION 2u
+#define SOLID_ABI_VERSION 3u
 #define SOLID_USER_NONE 0xFFFFFFFFu   /* "no user": sharer of an unflagged entry */
 
 typedef enum {
@@ -60,6 +60,15 @@ typedef struct {
   int32_t device;              /* CUDA device ordinal                                            */
   uint32_t world;              /* shards of the key-hash-partitioned index (1 = single GPU)      */
   uint32_t rank;               /* this context's shard, < world                                  */
+  uint32_t evict;              /* 0: a batch that would exceed capacity_blocks fails with
+                                  SOLID_ERR_CAPACITY (R9).  1: LRU eviction (SPEC evict_lru
+                                  S:117-125): after each request's inserts, while
+                                  more than capacity_blocks entries are live, the entry with the
+                                  smallest (last_used, key) is removed — last_used = the global
+                                  sequence number of the last request served it or inserted it
+                                  (R22-R25).  Single GPU only (world == 1); capacity_blocks >=
+                                  max_blocks.                                                     */
+  uint32_t reserved;           /* 0                                                              */
 } solid_config;
 
 typedef struct solid_ctx solid_ctx;
@@ -97,6 +106,14 @@ typedef struct {
   uint32_t sharer;   /* user that flagged it; AttackFlag <=> sharer != SOLID_USER_NONE (R5)  */
 } solid_entry;
 
+typedef struct {         /* solid_dump_ex (evict mode)                                        */
+  uint64_t key;
+  uint32_t owner;
+  uint32_t sharer;
+  uint64_t last_used;    /* LRU clock: global sequence number of the last request served it or
+                            that inserted it (R22)                                               */
+} solid_entry_ex;
+
 typedef struct {
   /* cumulative over all committed batches */
   uint64_t batches, requests, blocks, reused_blocks, inserted, flagged, diverted, truncated;
@@ -111,6 +128,16 @@ typedef struct {
   float ms_hash_kernel;          /* device time of k_hash_register alone (last batch)        */
   float ms_round_first;          /* device time of the resolver kernel (last batch)          */
   float round_us[8];             /* device time of resolver rounds 1..8 (globaltimer)        */
+  /* evict mode */
+  uint64_t evicted;              /* entries evicted, cumulative                              */
+  uint64_t last_evicted;         /* entries evicted by the last batch                        */
+  uint32_t last_evict_iters;     /* resolver / eviction-time iterations of the last batch    */
+  uint32_t last_window_keys;     /* batch keys in the eviction window (last batch)           */
+  uint64_t window_evicted;       /* cumulative: batch keys evicted by their own batch        */
+  uint32_t max_evict_iters;      /* max resolver / eviction-time iterations of any batch     */
+  uint32_t rebuilds;             /* index rebuilds (tombstone clean-up), cumulative          */
+  uint32_t compactions;          /* LRU log compactions, cumulative                          */
+  uint32_t reserved2;
 } solid_stats_t;
 
 uint32_t solid_abi_version(void);
@@ -127,7 +154,13 @@ solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* batch, solid_
                                 void* stream);
 
 /* Commit the staged admissions of the last lookup: 128-bit CAS claims {key, owner, sharer}
- * for new entries and sharer writes on flagged existing entries.  Checks capacity first. */
+ * for new entries and sharer writes on flagged existing entries.  Checks capacity first.
+ * Evict mode: also removes the batch's LRU victims (tombstones) and appends the LRU records of
+ * every entry the batch touched; a batch that would have to evict an entry it touched itself
+ * (it inserts more entries than the index holds untouched ones) fails with SOLID_ERR_CAPACITY
+ * and nothing is mutated — split it.  In evict mode solid_lookup_batch synchronises `stream`
+ * (the joint resolver / eviction-time iteration is host-driven) and
+ * solid_admit_batch is unavailable (SOLID_ERR_STATE). */
 solid_status solid_insert_batch(solid_ctx* ctx, void* stream);
 
 /* Asynchronous admission (lookup + insert with no host synchronisation), for a pipelined caller.
@@ -159,6 +192,10 @@ solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out);
 /* Copy live entries to host_out (HOST memory, capacity `cap` entries) sorted by key; *n_out =
  * number of live entries (may exceed cap; then only cap are written). */
 solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64_t cap, uint64_t* n_out);
+
+/* Evict mode: live entries with their LRU clock, sorted by key (as solid_dump).  Fails with
+ * SOLID_ERR_STATE on a context created with evict = 0. */
+solid_status solid_dump_ex(solid_ctx* ctx, solid_entry_ex* host_out, uint64_t cap, uint64_t* n_out);
 
 /* Empty the index (keeps allocations).  Synchronous, unless asynchronous batches are outstanding
  * (then ordered behind them on their stream, see solid_admit_batch). */

@@ -24,10 +24,12 @@ USER_NONE = 0xFFFFFFFF
 RESULT_DTYPE = np.dtype([("n_blocks", "<u4"), ("shared_hits", "<u4"), ("reused", "<u4"),
                          ("divert_at", "<i4"), ("flag_depth", "<u4"), ("bits", "<u4")])
 ENTRY_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4")])
+ENTRY_EX_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4"),
+                           ("last_used", "<u8")])
 
 # C ABI entry points declared in include/solid.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
-               "solid_insert_batch", "solid_admit_host", "solid_stats", "solid_dump",
+               "solid_insert_batch", "solid_admit_host", "solid_stats", "solid_dump", "solid_dump_ex",
                "solid_admit_batch", "solid_batch_status",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
@@ -49,7 +51,8 @@ class _Config(ctypes.Structure):
                 ("capacity_blocks", ctypes.c_uint64), ("max_batch_tokens", ctypes.c_uint64),
                 ("max_batch_requests", ctypes.c_uint64), ("hash_seed", ctypes.c_uint64),
                 ("policy", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32)]
+                ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32),
+                ("evict", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class _Batch(ctypes.Structure):
@@ -70,7 +73,12 @@ class _Stats(ctypes.Structure):
                 ("ms_resolve", ctypes.c_float), ("ms_commit", ctypes.c_float),
                 ("algorithmic_bytes", ctypes.c_uint64),
                 ("last_kernel_launches", ctypes.c_uint64), ("ms_hash_kernel", ctypes.c_float),
-                ("ms_round_first", ctypes.c_float), ("round_us", ctypes.c_float * 8)]
+                ("ms_round_first", ctypes.c_float), ("round_us", ctypes.c_float * 8),
+                ("evicted", ctypes.c_uint64), ("last_evicted", ctypes.c_uint64),
+                ("last_evict_iters", ctypes.c_uint32), ("last_window_keys", ctypes.c_uint32),
+                ("window_evicted", ctypes.c_uint64), ("max_evict_iters", ctypes.c_uint32),
+                ("rebuilds", ctypes.c_uint32), ("compactions", ctypes.c_uint32),
+                ("reserved2", ctypes.c_uint32)]
 
 
 class _ActConfig(ctypes.Structure):
@@ -113,6 +121,8 @@ def load_library(path: str = LIB_PATH):
     lib.solid_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
     lib.solid_dump.restype = st
     lib.solid_dump.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+    lib.solid_dump_ex.restype = st
+    lib.solid_dump_ex.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
     for name in ["solid_reset", "solid_checkpoint", "solid_restore"]:
         getattr(lib, name).restype = st
         getattr(lib, name).argtypes = [vp]
@@ -158,10 +168,13 @@ class Index:
     def __init__(self, policy: str = "solidarity", capacity_blocks: int = 1 << 20,
                  max_batch_tokens: int = 1 << 24, max_batch_requests: int = 1 << 16,
                  max_blocks: int = 8192, seed: int = 0x5011D000, device: int = 0,
-                 world: int = 1, rank: int = 0):
+                 world: int = 1, rank: int = 0, evict: bool = False):
+        """evict=True: LRU eviction at capacity_blocks instead of
+        SOLID_ERR_CAPACITY; lookup() then synchronises its stream."""
         self.lib = load_library()
         cfg = _Config(16, max_blocks, capacity_blocks, max_batch_tokens, max_batch_requests,
-                      seed & 0xFFFFFFFFFFFFFFFF, POLICY[policy], device, world, rank)
+                      seed & 0xFFFFFFFFFFFFFFFF, POLICY[policy], device, world, rank,
+                      1 if evict else 0, 0)
         self.world, self.rank = world, rank
         h = ctypes.c_void_p()
         rc = self.lib.solid_init(ctypes.byref(cfg), ctypes.byref(h))
@@ -276,6 +289,15 @@ class Index:
         out = np.zeros(max(int(n.value), 1), dtype=ENTRY_DTYPE)
         self._check(self.lib.solid_dump(self.h, ctypes.c_void_p(out.ctypes.data), n.value,
                                         ctypes.byref(n)))
+        return out[:int(n.value)]
+
+    def dump_ex(self) -> np.ndarray:
+        """Evict mode: live entries with their LRU clock (ENTRY_EX_DTYPE), sorted by key."""
+        n = ctypes.c_uint64()
+        self._check(self.lib.solid_dump_ex(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros(max(int(n.value), 1), dtype=ENTRY_EX_DTYPE)
+        self._check(self.lib.solid_dump_ex(self.h, ctypes.c_void_p(out.ctypes.data), n.value,
+                                           ctypes.byref(n)))
         return out[:int(n.value)]
 
     def reset(self):

@@ -21,6 +21,7 @@
 // keeps the EARLIEST request of the newest tag, so stale rounds and batches never need clearing.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>   // device radix sort / scan (LRU eviction mode, solid_evict.inc)
 
 #include <algorithm>
 #include <cstdint>
@@ -57,7 +58,7 @@ struct Cold {                         // the key and its index snapshot at batch
   uint32_t snap_owner;                // kNone = absent from the index
   uint32_t snap_sharer;
   uint32_t psl;                       // index slot (snapshot entry, or the slot claimed at commit)
-  uint32_t pad;
+  uint32_t win;                       // evict mode: eviction-window index, kNone = not in it
 };
 static_assert(sizeof(Hot) == 32 && sizeof(Cold) == 24, "layout");
 
@@ -114,6 +115,24 @@ struct KParams {
   unsigned long long* int_ins;     // per local id: this round's earliest local inserter (seq'<<32|user)
   unsigned long long* int_flg;     // per local id: this round's earliest local flagger
   uint32_t* mown;                  // per local id: owner user of the mirrored first inserter
+  // LRU eviction mode (solid_evict.inc): keys of the batch whose LRU record lies
+  // in the eviction window get a window index w (their index snapshot is then visible only up
+  // to their eviction time win_ev[w]); winfo[id] = epoch << 32 | w publishes an id's creation
+  int evict;
+  unsigned long long* winfo;
+  const uint32_t* lpos;            // per index slot: position of its valid LRU record
+  const uint32_t* lbits;           // LRU log valid bitmap
+  const uint32_t* lpc;             // exclusive prefix popcount of lbits words (batch start)
+  const unsigned long long* sum_blocks;   // sum of n_j over the batch (device)
+  unsigned long long ev_live0, ev_cap;
+  uint32_t* win_cnt;
+  uint32_t* win_id;
+  uint32_t* win_rank;
+  uint32_t* win_ev;                // seq' of the evicting request, kNone = not evicted
+  unsigned long long* win_oflg;    // [w][2] old-incarnation flagger (tagged, ping-pong)
+  uint32_t* win_tau;               // first request served the key (post-pass)
+  uint32_t* ins_cnt;               // per request: entries it inserts (final round)
+  uint32_t* lt;                    // per id: last request served it (final)
 };
 
 #define POLICY_IS_SOLIDARITY(kp) ((kp).policy == SOLID_POLICY_SOLIDARITY)
@@ -194,7 +213,7 @@ __device__ __forceinline__ bool index_find_from(const KParams& kp, uint64_t key,
       sharer = (uint32_t)(e.y >> 32);
       return true;
     }
-    if (e.x == 0) return false;
+    if (e.x == 0 && e.y == 0) return false;   // EMPTY; {0, ~0} is a tombstone (evict mode)
     pos = (pos + 1) & kp.tmask;
     e = ldw128(&kp.tab[pos]);
   }
@@ -220,9 +239,30 @@ __device__ __forceinline__ bool init_id_at(const KParams& kp, uint32_t id, uint6
   c.snap_owner = present ? owner : kNone;
   c.snap_sharer = present ? sharer : kNone;
   c.psl = present ? (uint32_t)ipos : kNone;
-  c.pad = 0;
+  c.win = kNone;
+  if (kp.evict && present) {
+    // eviction window: the entry's LRU rank among the live entries at batch start
+    // (valid records before its own); only ranks below ebound can be evicted by this batch
+    const uint32_t p = kp.lpos[ipos];
+    const uint32_t rank = kp.lpc[p >> 5] + __popc(kp.lbits[p >> 5] & ((1u << (p & 31)) - 1u));
+    const unsigned long long tot = kp.ev_live0 + *kp.sum_blocks;
+    const unsigned long long ebound = tot > kp.ev_cap ? tot - kp.ev_cap : 0ull;
+    if (rank < ebound) {
+      const uint32_t w = atomicAdd(kp.win_cnt, 1u);
+      kp.win_id[w] = id;
+      kp.win_rank[w] = rank;
+      kp.win_ev[w] = kNone;
+      kp.win_oflg[2 * w] = ~0ull;
+      kp.win_oflg[2 * w + 1] = ~0ull;
+      c.win = w;
+    }
+#ifdef SOLID_EVDEBUG
+    printf("init id %u key %llx slot %llu p %u rank %u ebound %llu w %u\n", id,
+           (unsigned long long)key, (unsigned long long)ipos, p, rank, ebound, c.win);
+#endif
+  }
   kp.cold[id] = c;
-  if (present) {
+  if (present && c.win == kNone) {
     Hot* h = kp.hot + id;
     const unsigned long long v = (unsigned long long)tag_of(kp.epoch, kSubSnap) << 32;
     atomicMin(&h->v[0], v);
@@ -231,6 +271,10 @@ __device__ __forceinline__ bool init_id_at(const KParams& kp, uint32_t id, uint6
       atomicMin(&h->v[1], v);
       atomicMin(&h->v[3], v);
     }
+  }
+  if (kp.evict) {              // publish: readers wait for epoch << 32 | w before reading state
+    __threadfence();
+    atomicExch(&kp.winfo[id], ((unsigned long long)kp.epoch << 32) | c.win);
   }
   return present;
 }
@@ -997,6 +1041,8 @@ struct solid_ctx {
   // sharded mode (solid_dist.inc)
   struct Dist* dist = nullptr;
   uint64_t last_add = 0;
+  // LRU eviction mode (solid_evict.inc)
+  struct Evict* ev_state = nullptr;
 };
 
 static void set_slot(solid_ctx* c, uint32_t i) {
@@ -1033,7 +1079,16 @@ extern "C" const char* solid_last_error(const solid_ctx* ctx) {
   return ctx ? ctx->err.c_str() : "null context";
 }
 
+static void evict_free(solid_ctx* ctx);
+static solid_status evict_init(solid_ctx* ctx);
+static solid_status evict_lookup(solid_ctx* ctx, cudaStream_t s);
+static solid_status evict_insert(solid_ctx* ctx, cudaStream_t s);
+static solid_status evict_reset(solid_ctx* ctx, cudaStream_t s);
+static solid_status evict_checkpoint(solid_ctx* ctx);
+static solid_status evict_restore(solid_ctx* ctx);
+
 static void free_all(solid_ctx* c) {
+  evict_free(c);
   cudaFree(c->tab);
   cudaFree(c->tab_ckpt);
   cudaFree(c->stab);
@@ -1085,6 +1140,8 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
     return SOLID_ERR_INVALID;
   const uint32_t world = cfg->world ? cfg->world : 1;
   if (world > 64 || cfg->rank >= world) return SOLID_ERR_INVALID;
+  if (cfg->evict > 1 || (cfg->evict && (world != 1 || cfg->capacity_blocks < cfg->max_blocks)))
+    return SOLID_ERR_INVALID;
   ctx = new solid_ctx();
   ctx->cfg = *cfg;
   ctx->cfg.world = world;
@@ -1150,6 +1207,14 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   for (auto& f : ctx->fl)
     for (auto& e : f.ev) CK(cudaEventCreate(&e));
   set_slot(ctx, 0);
+  if (cfg->evict) {
+    rc = evict_init(ctx);
+    if (rc != SOLID_OK) {
+      free_all(ctx);
+      delete ctx;
+      return rc;
+    }
+  }
   if (world > 1) {
     rc = dist_init(ctx, world, cfg->rank);
     if (rc != SOLID_OK) {
@@ -1260,6 +1325,7 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   kp.st = ctx->st;
   CK(cudaMemsetAsync(ctx->st, 0, sizeof(DevStatus), s));
   CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
+  if (ctx->ev_state) return evict_lookup(ctx, s);
   CK(cudaEventRecord(ctx->ev[0], s));
   const uint64_t n = b->n_requests;
   ctx->launches = 0;
@@ -1406,6 +1472,7 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   if (!ctx->pending) return fail(ctx, SOLID_ERR_STATE, "insert_batch without a pending lookup");
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(ctx->dev));
+  if (ctx->ev_state) return evict_insert(ctx, s);
   solid_status rc = enqueue_commit(ctx, s, false);
   if (rc != SOLID_OK) return rc;
   CK(cudaStreamSynchronize(s));
@@ -1416,6 +1483,8 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
 extern "C" solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch,
                                           solid_result* out, void* stream) {
   if (!ctx) return SOLID_ERR_INVALID;
+  if (ctx->ev_state)
+    return fail(ctx, SOLID_ERR_STATE, "evict mode: admission is synchronous (lookup + insert)");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "admit_batch with a pending lookup");
   if (ctx->outstanding == kRing)
     return fail(ctx, SOLID_ERR_STATE,
@@ -1550,6 +1619,10 @@ extern "C" solid_status solid_reset(solid_ctx* ctx) {
     solid_status rc = init_scratch(ctx, s);
     if (rc != SOLID_OK) return rc;
   }
+  if (ctx->ev_state) {
+    solid_status rc = evict_reset(ctx, s);
+    if (rc != SOLID_OK) return rc;
+  }
   CK(cudaMemsetAsync(ctx->live_dev, 0, sizeof(unsigned long long), s));
   if (!ctx->outstanding) CK(cudaStreamSynchronize(s));
   if (ctx->poisoned) ctx->head = ctx->outstanding = 0;   // their results are lost with the state
@@ -1568,6 +1641,8 @@ extern "C" solid_status solid_checkpoint(solid_ctx* ctx) {
   if (rc0 != SOLID_OK) return rc0;
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+  ctx->live_ckpt = ctx->live;
+  if (ctx->ev_state) return evict_checkpoint(ctx);
   if (!ctx->tab_ckpt) CK(cudaMalloc(&ctx->tab_ckpt, ctx->tcap * sizeof(ulonglong2)));
   CK(cudaMemcpy(ctx->tab_ckpt, ctx->tab, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToDevice));
   ctx->live_ckpt = ctx->live;
@@ -1576,12 +1651,19 @@ extern "C" solid_status solid_checkpoint(solid_ctx* ctx) {
 
 extern "C" solid_status solid_restore(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
-  if (!ctx->tab_ckpt) return fail(ctx, SOLID_ERR_STATE, "restore without checkpoint");
+  if (!ctx->tab_ckpt && !ctx->ev_state) return fail(ctx, SOLID_ERR_STATE, "restore without checkpoint");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "restore with a pending batch");
   solid_status rc0 = require_collected(ctx, "restore");
   if (rc0 != SOLID_OK) return rc0;
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->ev_state) {
+    solid_status rc = evict_restore(ctx);
+    if (rc != SOLID_OK) return rc;
+    ctx->live = ctx->live_ckpt;
+    CK(cudaMemcpy(ctx->live_dev, &ctx->live, sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    return SOLID_OK;
+  }
   CK(cudaMemcpy(ctx->tab, ctx->tab_ckpt, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToDevice));
   ctx->live = ctx->live_ckpt;
   CK(cudaMemcpy(ctx->live_dev, &ctx->live, sizeof(unsigned long long), cudaMemcpyHostToDevice));
@@ -1589,3 +1671,4 @@ extern "C" solid_status solid_restore(solid_ctx* ctx) {
 }
 
 #include "solid_dist.inc"
+#include "solid_evict.inc"

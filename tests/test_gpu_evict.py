@@ -1,0 +1,157 @@
+"""GPU parity of LRU eviction: the CUDA evict mode through the
+C ABI against the oracle with the same capacity, bit-exact on every result field and on the
+final index including each entry's LRU clock (key, owner, sharer, last_used), for every policy
+and batch partition.  A batch the GPU rejects because it would evict entries it touched itself
+(SOLID_ERR_CAPACITY, nothing mutated) is split in halves, as a caller would."""
+import numpy as np
+import pytest
+
+from oracle import Oracle
+from workloads import c1_tiny, c3_multiturn, concat_streams, random_small
+
+pytestmark = pytest.mark.gpu
+SEED = 0x5011D000
+POL = {"apc": 0, "user_isolation": 1, "solidarity": 2}
+
+
+def _index(policy, streams, capacity, max_blocks):
+    import paper_2603_10726_b200 as P
+    tok = max(max(s.n_tokens for s in streams), 64)
+    req = max(max(s.n_requests for s in streams), 1)
+    return P.Index(policy, capacity_blocks=capacity, max_batch_tokens=tok + 64,
+                   max_batch_requests=req, max_blocks=max_blocks, seed=SEED, evict=True)
+
+
+def _admit_split(idx, s, splits):
+    """Admit s; on SOLID_ERR_CAPACITY (the batch would evict entries it touched) split it."""
+    import torch
+    import paper_2603_10726_b200 as P
+    try:
+        out = P.as_numpy(idx.admit(**P.to_device(s)))
+        torch.cuda.synchronize()
+        return out
+    except P.SolidError as e:
+        if e.status != P.SOLID_ERR_CAPACITY or s.n_requests < 2:
+            raise
+        splits.append(s.n_requests)
+        h = s.n_requests // 2
+        return np.concatenate([_admit_split(idx, s.slice(0, h), splits),
+                               _admit_split(idx, s.slice(h, s.n_requests), splits)])
+
+
+def _batches(s, size):
+    return [s.slice(i, min(i + size, s.n_requests)) for i in range(0, s.n_requests, size)]
+
+
+def run_both(stream, policy, capacity, batch, max_blocks=64, warm=None):
+    o = Oracle(16, SEED, POL[policy], capacity=capacity)
+    streams = ([warm] if warm is not None else []) + [stream]
+    parts = [_batches(s, batch) for s in streams]
+    idx = _index(policy, [b for p in parts for b in p], capacity, max_blocks)   # batch-sized scratch
+    splits = []
+    got, exp = [], []
+    for s, p in zip(streams, parts):
+        exp.append(o.process(s))
+        for b in p:
+            got.append(_admit_split(idx, b, splits))
+    got, exp = np.concatenate(got), np.concatenate(exp)
+    for f in exp.dtype.names:
+        bad = np.nonzero(got[f].astype(np.int64) != exp[f].astype(np.int64))[0]
+        assert bad.size == 0, (f, bad[:5], got[bad[:5]], exp[bad[:5]])
+    gd, ed = idx.dump_ex(), o.dump_ex()
+    assert len(gd) == len(ed) == o.size() <= capacity
+    for f in ["key", "owner", "sharer", "last_used"]:
+        assert np.array_equal(gd[f], ed[f]), f
+    st = idx.stats()
+    assert st["evicted"] == o.evictions()
+    assert st["live_entries"] == o.size()
+    return st, splits, o
+
+
+@pytest.mark.parametrize("policy", ["apc", "user_isolation", "solidarity"])
+@pytest.mark.parametrize("capacity", [8, 13, 40])
+@pytest.mark.parametrize("batch", [1, 7, 64, 1000])
+def test_random_streams_lru(policy, capacity, batch):
+    for seed in (1, 2, 3):
+        s = random_small(300, users=1 + seed, alphabet_blocks=3, max_blocks=6, seed=seed,
+                         enforce_prob=0.8 if seed % 2 else 1.0)
+        st, _, o = run_both(s, policy, capacity, batch, max_blocks=8)
+        assert o.evictions() > 0
+
+
+@pytest.mark.parametrize("policy", ["apc", "solidarity"])
+def test_c1_tiny_under_pressure(policy):
+    s = c1_tiny()
+    for cap in (40, 100, 300):
+        run_both(s, policy, cap, 16, max_blocks=32)
+
+
+@pytest.mark.parametrize("policy", ["apc", "user_isolation", "solidarity"])
+def test_multiturn_under_pressure(policy):
+    """C3-shaped conversations with a cache far smaller than the working set: the window keys
+    (returning conversations whose prefix is about to be evicted) are the coupled case."""
+    warm, timed = c3_multiturn(users=60, warm_blocks=3000, timed_rounds=6, seed=11)
+    st, splits, o = run_both(timed, policy, 1500, 60, max_blocks=512, warm=warm)
+    assert o.evictions() > 1000
+    assert st["window_evicted"] > 0
+
+
+def test_window_keys_are_exercised():
+    """A stream built so that requests revisit entries the same batch evicts: a shared prefix
+    revisited after enough fresh traffic, all in one batch."""
+    from oracle_helpers import Blocks
+    from workloads.gen import _pack
+    B = Blocks(seed=21)
+    prompts, users = [], []
+    for i in range(12):
+        prompts.append(B.prompt([f"p{i}a", f"p{i}b"]))
+        users.append(i % 3)
+    for rep in range(3):
+        for i in range(12):
+            prompts.append(B.prompt([f"p{i}a", f"p{i}b", f"x{rep}{i}"]))
+            users.append((i + rep) % 4)
+    s = _pack("revisit", prompts, users)
+    coupled = 0
+    for cap in (8, 10, 16, 25):
+        for pol in ("apc", "solidarity"):
+            st, splits, o = run_both(s.slice(12, s.n_requests), pol, cap, 64, max_blocks=8,
+                                     warm=s.slice(0, 12))
+            coupled += st["window_evicted"] > 0 and st["max_evict_iters"] >= 2
+    assert coupled > 0
+
+
+def test_rebuild_and_compaction():
+    """Many batches through a small cache: tombstones trigger table rebuilds and the LRU log is
+    compacted; the final state still equals the oracle's."""
+    s = random_small(400000, users=6, alphabet_blocks=400, max_blocks=6, seed=9)
+    st, _, _ = run_both(s, "solidarity", 4000, 4000, max_blocks=8)
+    assert st["rebuilds"] >= 1 and st["compactions"] >= 1, st
+
+
+def test_evict_rejects_bad_config_and_async():
+    import paper_2603_10726_b200 as P
+    with pytest.raises(P.SolidError):
+        P.Index("apc", capacity_blocks=4, max_blocks=8, evict=True)     # capacity < max_blocks
+    idx = P.Index("apc", capacity_blocks=64, max_batch_tokens=1 << 12, max_batch_requests=64,
+                  max_blocks=8, evict=True)
+    s = random_small(10, users=2, alphabet_blocks=3, max_blocks=4, seed=1)
+    with pytest.raises(P.SolidError):
+        idx.admit_async(**P.to_device(s))
+    idx.admit(**P.to_device(s))   # the synchronous path still works after the refusal
+
+
+def test_checkpoint_restore_evict():
+    import torch
+    import paper_2603_10726_b200 as P
+    s = random_small(400, users=3, alphabet_blocks=5, max_blocks=6, seed=4)
+    a, b = s.slice(0, 200), s.slice(200, 400)
+    idx = P.Index("solidarity", capacity_blocks=20, max_batch_tokens=1 << 16,
+                  max_batch_requests=256, max_blocks=8, seed=SEED, evict=True)
+    _admit_split(idx, a, [])
+    idx.checkpoint()
+    r1 = _admit_split(idx, b, [])
+    d1 = idx.dump_ex()
+    idx.restore()
+    r2 = _admit_split(idx, b, [])
+    torch.cuda.synchronize()
+    assert np.array_equal(r1, r2) and np.array_equal(d1, idx.dump_ex())
