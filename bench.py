@@ -191,6 +191,90 @@ def measure_activator(dev, args):
     return out
 
 
+def measure_evict(dev, args):
+    """LRU eviction (evict mode) on the C3 multi-turn shape
+    (BASELINE configs[2]: 10k users, conversations growing to 8k tokens) with the index capped
+    at 1M entries: warmed (untimed, on the GPU) until the cache is full and evicting, then one
+    step = one batch of 2 000 requests (a fifth of a round) admitted with lookup + insert,
+    index restored to the same warm state before every step (outside the events)."""
+    import torch
+    import paper_2603_10726_b200 as P
+    from workloads import c3_multiturn
+    cap, users, bsz = 1_000_000, 10_000, 2_000
+    warm, timed = c3_multiturn(users=users, warm_blocks=cap, timed_rounds=1, seed=SEED + 3)
+    batch = timed.slice(0, bsz)
+    wb = [warm.slice(i, min(i + bsz, warm.n_requests)) for i in range(0, warm.n_requests, bsz)]
+    max_tok = max(max(b.n_tokens for b in wb), batch.n_tokens) + 64
+    idx = P.Index("solidarity", capacity_blocks=cap, max_batch_tokens=max_tok,
+                  max_batch_requests=bsz, seed=SEED, device=dev.index or 0, evict=True)
+
+    def admit_split(b):
+        try:
+            idx.admit(**P.to_device(b, dev))
+        except P.SolidError as e:
+            if e.status != P.SOLID_ERR_CAPACITY or b.n_requests < 2:
+                raise
+            h = b.n_requests // 2
+            admit_split(b.slice(0, h)); admit_split(b.slice(h, b.n_requests))
+    t0 = time.perf_counter()
+    for b in wb:
+        admit_split(b)
+    warm_s = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    idx.checkpoint()
+    d = P.to_device(batch, dev)
+    out = torch.empty((bsz, 6), dtype=torch.int32, device=dev)
+    cs = torch.cuda.current_stream(dev)
+    ms, st = [], None
+    prof = os.environ.get("SOLID_PROFILE_EVICT")   # ncu --profile-from-start off: last step only
+    nsteps = args.warmup + max(args.steps, 3)
+    for k in range(nsteps):
+        idx.restore()
+        torch.cuda.synchronize()
+        if prof and k == nsteps - 1:
+            torch.cuda.profiler.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        idx.lookup(d["tokens"], d["offsets"], d["users"], None, out=out)
+        idx.insert()
+        e1.record(cs)
+        torch.cuda.synchronize()
+        if prof and k == nsteps - 1:
+            torch.cuda.profiler.stop()
+        if k >= args.warmup:
+            ms.append(e0.elapsed_time(e1))
+            st = idx.stats()
+    med = statistics.median(ms)
+    nblk = batch.n_blocks()
+    res = P.as_numpy(out)
+    r = {"workload": f"c3_multiturn {users} users, index capped at {cap} entries (LRU), warmed "
+                     f"with {warm.n_requests} requests ({warm.n_blocks()} blocks) until full; "
+                     f"one batch = {bsz} requests ({nblk} blocks, {batch.n_tokens} tokens)",
+         "ms_per_batch": med, "ms_all": ms, "requests_per_s": bsz / (med / 1e3),
+         "blocks_per_s": nblk / (med / 1e3), "evicted_per_batch": st["last_evicted"],
+         "inserted_per_batch": st["last_inserted"], "reused_blocks": int(res["reused"].sum()),
+         "window_keys": st["last_window_keys"], "evict_iterations": st["last_evict_iters"],
+         "resolver_rounds": st["last_rounds"], "launches_per_batch": st["last_kernel_launches"],
+         "phases_ms": {"hash": st["ms_hash"], "resolve_and_window": st["ms_resolve"],
+                       "commit_evict_lru": st["ms_commit"]},
+         "live_entries": st["live_entries"], "warm_wall_s": warm_s,
+         "how": "lookup (synchronises: host-driven eviction-time iteration) + insert, CUDA "
+                "events on the stream around both, median"}
+    if not args.no_cpu:
+        from oracle import Oracle
+        sample = warm.slice(0, 6000)
+        o = Oracle(16, SEED, 2, capacity=20_000)
+        t0 = time.perf_counter()
+        o.process(sample)
+        dt = time.perf_counter() - t0
+        r["cpu_baseline"] = {"value": sample.n_requests / dt, "unit": "requests/s", "cores": 1,
+                             "kind": "oracle", "blocks_per_s": sample.n_blocks() / dt,
+                             "sample": f"first {sample.n_requests} warm requests "
+                                       f"({sample.n_blocks()} blocks) with capacity 20 000 "
+                                       f"(evicting: {o.evictions()} evictions), 1 thread"}
+    return r
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -356,6 +440,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=20_000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-activator", action="store_true")
+    ap.add_argument("--no-evict", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
@@ -498,6 +583,10 @@ def main():
     if rank == 0 and world == 1 and not args.profile and not args.no_activator:
         activator = measure_activator(dev, args)
 
+    lru = None
+    if rank == 0 and world == 1 and not args.profile and not args.no_evict:
+        lru = measure_evict(dev, args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
         cpu = cpu_baseline(stream_np, args.cpu_sample)
@@ -522,6 +611,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "activator": activator,
+            "lru_eviction": lru,
             "e2e": e2e,
             "gpu_launches": int(sum(launches)),
             "clocks": clocks,
