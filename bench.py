@@ -275,6 +275,49 @@ def measure_evict(dev, args):
     return r
 
 
+def measure_policy_eval(dev, args):
+    """hit rates of the three policies on W1-W5 (P:744-772, 10 users x 100
+    requests, single- and two-level templates) and the θ sweep on two-level W4, the
+    CUDA library as the cache and the CUDA Activator in the loop (workloads/policy_eval.py)."""
+    import torch
+    import paper_2603_10726_b200 as P
+    from workloads.policy_eval import PRESETS, closed_loop, hit_rate, preset, two_level
+
+    def admit_fn(policy, s):
+        idx = P.Index(policy, capacity_blocks=1 << 16, max_batch_tokens=s.n_tokens + 64,
+                      max_batch_requests=s.n_requests, seed=SEED, device=dev.index or 0)
+        return lambda b: P.as_numpy(idx.admit(**P.to_device(b, dev)))
+    t0 = time.perf_counter()
+    table = {}
+    for gname, gen in (("single", preset), ("two_level", two_level)):
+        for w in PRESETS:
+            s = gen(w)
+            row = {}
+            for pol in ("apc", "user_isolation", "solidarity"):
+                a = admit_fn(pol, s)
+                res = np.concatenate([a(s.slice(i, min(i + 100, s.n_requests)))
+                                      for i in range(0, s.n_requests, 100)])
+                row[pol] = round(hit_rate(res), 4)
+            table[f"{gname}:{w}"] = row
+    s = two_level("W4")
+    d = lambda a, t: torch.from_numpy(np.ascontiguousarray(a)).to(dtype=t, device=dev)
+    sweep = {}
+    for th in np.linspace(0.0, 1.0, 11):
+        act = P.Activator(theta=float(th), max_samples=s.n_requests + 1, max_queries=64,
+                          device=dev.index or 0)
+        fn = lambda tt, pt, fr, c: act.run(d(tt, torch.float64), d(pt.astype(np.int32), torch.int32),
+                                           d(fr, torch.float64), d(c, torch.int64))[1].cpu().numpy()
+        res, en, _ = closed_loop(s, admit_fn("solidarity", s), fn, batch=50)
+        sweep[f"{th:.1f}"] = {"hit_rate": round(hit_rate(res), 4),
+                              "enforced": round(float(en.mean()), 3)}
+    return {"workloads": "W1-W5 presets (10 users x 100 requests, seed 0x5011D0F3); two_level = "
+                         "templates in families of 8 sharing a 3-block preamble",
+            "hit_rates": table, "theta_sweep_two_level_W4": sweep,
+            "wall_s": time.perf_counter() - t0,
+            "how": "library admission in batches of 100 (sweep: 50, Activator windows of the "
+                   "samples completed before each batch; synthetic TTFT stand-in)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -441,6 +484,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-activator", action="store_true")
     ap.add_argument("--no-evict", action="store_true")
+    ap.add_argument("--no-policy-eval", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
@@ -587,6 +631,10 @@ def main():
     if rank == 0 and world == 1 and not args.profile and not args.no_evict:
         lru = measure_evict(dev, args)
 
+    peval = None
+    if rank == 0 and world == 1 and not args.profile and not args.no_policy_eval:
+        peval = measure_policy_eval(dev, args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
         cpu = cpu_baseline(stream_np, args.cpu_sample)
@@ -612,6 +660,7 @@ def main():
             "cpu_baseline": cpu,
             "activator": activator,
             "lru_eviction": lru,
+            "policy_eval": peval,
             "e2e": e2e,
             "gpu_launches": int(sum(launches)),
             "clocks": clocks,

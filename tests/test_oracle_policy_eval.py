@@ -1,0 +1,88 @@
+"""Policy evaluation: the paper's §6.2.1 workload claims and the
+§6.3 threshold sweep as properties of the oracle on the W1-W5 workloads
+(workloads/policy_eval.py; SPEC acceptance criteria 3-4).  CPU, seconds."""
+import numpy as np
+import pytest
+
+from oracle import Oracle, POLICY_APC, POLICY_SOLIDARITY, POLICY_USER_ISOLATION
+from oracle.activator import ActivatorConfig, enforce_stream
+from workloads.policy_eval import PRESETS, closed_loop, hit_rate, preset, two_level
+
+SEED = 0x5011D000
+
+
+def _run(s, pol):
+    return Oracle(16, SEED, pol).process(s)
+
+
+def test_generator_is_deterministic():
+    a, b = preset("W3"), preset("W3")
+    assert np.array_equal(a.tokens, b.tokens) and np.array_equal(a.users, b.users)
+    assert not np.array_equal(preset("W3", seed=7).tokens[:4096], a.tokens[:4096])
+
+
+def test_w1_all_policies_equal():
+    """W1 (high intra, zero inter): 'all baselines behave similarly' — here exactly: no
+    prefix crosses a user boundary, so every policy reuses the same blocks (I8)."""
+    s = preset("W1")
+    r = [_run(s, p)["reused"] for p in (POLICY_APC, POLICY_USER_ISOLATION, POLICY_SOLIDARITY)]
+    assert np.array_equal(r[0], r[1]) and np.array_equal(r[0], r[2])
+    assert hit_rate(_run(s, POLICY_APC)) > 0.5
+
+
+def test_w5_user_isolation_zero_solidarity_close_to_apc():
+    """W5 (zero intra, high inter): 'User Cache Isolation has zero cache hit rate';
+    CacheSolidarity's hit rate 'similarly high' to Prefix Caching (SPEC: within 5 points)."""
+    s = preset("W5")
+    assert hit_rate(_run(s, POLICY_USER_ISOLATION)) == 0.0
+    apc, cs = hit_rate(_run(s, POLICY_APC)), hit_rate(_run(s, POLICY_SOLIDARITY))
+    assert apc > 0.2 and apc - cs <= 0.05
+
+
+@pytest.mark.parametrize("gen", [preset, two_level])
+@pytest.mark.parametrize("w", list(PRESETS))
+def test_policy_dominance(gen, w):
+    """hit_rate(UserIsolation) <= hit_rate(CacheSolidarity) + 0.01 and CacheSolidarity
+    never reuses more than Prefix Caching, request by request (I4)."""
+    s = gen(w)
+    apc, ui, cs = (_run(s, p) for p in (POLICY_APC, POLICY_USER_ISOLATION, POLICY_SOLIDARITY))
+    assert hit_rate(ui) <= hit_rate(cs) + 0.01
+    assert (cs["reused"] <= apc["reused"]).all()
+
+
+def test_two_level_sharing_costs_reuse_between_the_baselines():
+    """With templates that share a preamble, selective isolation diverts requests whose next
+    entry belongs to another user: CacheSolidarity lands strictly between the baselines on W2-W4
+    (P:759-760, P:765 'performs between the two baselines')."""
+    for w in ("W2", "W3", "W4"):
+        s = two_level(w)
+        apc, ui, cs = (hit_rate(_run(s, p)) for p in (POLICY_APC, POLICY_USER_ISOLATION,
+                                                     POLICY_SOLIDARITY))
+        assert ui < cs < apc, (w, ui, cs, apc)
+
+
+def _sweep_point(s, theta):
+    cfg = ActivatorConfig(theta=float(theta))
+    o = Oracle(16, SEED, POLICY_SOLIDARITY)
+    act = lambda tt, pt, fr, cuts: enforce_stream(tt, pt, fr, cuts, cfg)[0]
+    return closed_loop(s, lambda b: o.process(b), act, batch=50)
+
+
+def test_theta_sweep_endpoints_and_trend():
+    """§6.3 / fig:kde_threshold_results: θ = 0 gives Prefix Caching's
+    reuse request by request (isolation never enforced once windows exist, flags still written),
+    θ = 1 the detector-always-on reuse; the hit rate is non-increasing in θ up to 1 point."""
+    s = two_level("W4")
+    apc = _run(s, POLICY_APC)
+    always = _run(s, POLICY_SOLIDARITY)
+    hr = []
+    for th in np.linspace(0.0, 1.0, 11):
+        res, en, _ = _sweep_point(s, th)
+        hr.append(hit_rate(res))
+        if th == 0.0:
+            assert np.array_equal(res["reused"], apc["reused"])
+            assert en[50:].sum() == 0               # only the fail-safe first batch enforces
+        if th == 1.0:
+            assert np.array_equal(res["reused"], always["reused"]) and en.all()
+    assert hr[0] > hr[-1]
+    assert all(b <= a + 0.01 for a, b in zip(hr, hr[1:])), hr

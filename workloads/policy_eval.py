@@ -14,7 +14,7 @@ the paper gives levels only); presets W1 = (High intra, Zero inter), W2 =
 Moderate), W3 = (Moderate, Moderate), W4 = (High, High), W5 = (Zero, High) (W1, W2,
 W5 from the §6.2.1 prose); per request: with p_intra repeat one of the user's own earlier stems,
 else with p_inter adopt a shared template the user has not used yet, else a fresh stem (S:378);
-the per-user secret slot sits in the middle of the stem (S:366 secret_position Middle); arrival
+the per-user secret slot sits late in the stem (block 6 of 8; S:366 secret_position); arrival
 order is a seeded merge of per-user Poisson processes (order only).
 """
 from __future__ import annotations
@@ -32,10 +32,15 @@ K_TEMPLATE, K_SECRET, K_FRESH, K_QTAIL = 41, 42, 43, 44
 
 
 def reuse_workload(intra: str, inter: str, users: int = 10, requests_per_user: int = 100,
-                   stem_blocks: int = 8, secret_at: int = 4, templates: int = 64,
+                   stem_blocks: int = 8, secret_at: int = 6, templates: int = 64,
+                   family_size: int = 1, family_blocks: int = 3,
                    seed: int = 0x5011D0F3, block_size: int = 16, vocab: int = VOCAB) -> Stream:
     """One §6.2.1 workload: each prompt = stem (stem_blocks blocks, block `secret_at` replaced
-    by the user's secret block) + a fresh query (1-3 blocks plus a partial tail)."""
+    by the user's secret block) + a fresh query (1-3 blocks plus a partial tail).  Shared
+    templates may come in families of `family_size` whose first `family_blocks` blocks coincide
+    (a task preamble shared by several templates: two-level inter-user sharing, where selective
+    isolation costs reuse); the W1-W5 presets use single templates (family_size 1), the θ sweep
+    the two-level variant."""
     rng = np.random.default_rng(seed)
     p_intra, p_inter = LEVELS[intra], LEVELS[inter]
     bs = block_size
@@ -64,7 +69,8 @@ def reuse_workload(intra: str, inter: str, users: int = 10, requests_per_user: i
                 if b == secret_at:
                     blocks.append(secret[u])
                 elif stem[0] == "T":
-                    blocks.append(run(seed, K_TEMPLATE, stem[1] * 1024 + b, bs, vocab))
+                    tid = (stem[1] // family_size) * 4096 if b < family_blocks else stem[1]
+                    blocks.append(run(seed, K_TEMPLATE, tid * 1024 + b, bs, vocab))
                 else:
                     blocks.append(run(seed, K_FRESH, stem[1] * 1024 + b, bs, vocab))
             qn = int(rng.integers(bs, 3 * bs + 1)) + int(rng.integers(1, bs))
@@ -124,10 +130,9 @@ def closed_loop(stream: Stream, admit: Callable, activator: Optional[Callable], 
         b = stream.slice(lo, hi)
         if enforce_override is not None:
             enforce[lo:hi] = enforce_override[lo:hi]
-        elif activator is not None:
+        elif activator is not None and lo > 0:   # no samples yet: fail-safe enforce (R21)
             cuts = np.full(hi - lo, lo, np.int64)
-            enforce[lo:hi] = activator(ttft[:max(lo, 1)], ptok[:max(lo, 1)], frac[:max(lo, 1)],
-                                       cuts)
+            enforce[lo:hi] = activator(ttft[:lo], ptok[:lo], frac[:lo], cuts)
         b.enforce = np.ascontiguousarray(enforce[lo:hi])
         res = admit(b)
         out.append(res)
@@ -135,3 +140,10 @@ def closed_loop(stream: Stream, admit: Callable, activator: Optional[Callable], 
         frac[lo:hi] = np.where(nb > 0, res["reused"] / np.maximum(nb, 1), 0.0)
         ttft[lo:hi] = synthetic_ttft_ms(ptok[lo:hi], res["reused"].astype(np.float64), rng)
     return np.concatenate(out), enforce, (ttft, ptok, frac)
+
+
+def two_level(name: str, **kw) -> Stream:
+    """A preset with two-level templates (families of 8 sharing a 3-block preamble)."""
+    kw.setdefault("family_size", 8)
+    kw.setdefault("family_blocks", 3)
+    return preset(name, **kw)
