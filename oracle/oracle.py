@@ -68,6 +68,10 @@ def _load():
         lib.oracle_evictions.argtypes = [vp]
         lib.oracle_next_seq.restype = u64
         lib.oracle_next_seq.argtypes = [vp]
+        lib.oracle_set_components.restype = ctypes.c_int
+        lib.oracle_set_components.argtypes = [vp, ctypes.c_int]
+        lib.oracle_params2.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        lib.oracle_chain2.argtypes = [vp, vp, u32, u32, i32, vp, vp, vp]
         lib.oracle_dump_ex.restype = u64
         lib.oracle_dump_ex.argtypes = [vp, vp, u64]
         _lib = lib
@@ -82,13 +86,16 @@ class Oracle:
     """Sequential reference: Oracle(block_size, seed, policy).process(stream) -> results."""
 
     def __init__(self, block_size: int = 16, seed: int = 0, policy: int = POLICY_SOLIDARITY,
-                 capacity: int = 0):
+                 capacity: int = 0, components: int = 1):
         self.lib = _load()
         self.block_size, self.seed, self.policy = block_size, seed, policy
         self.h = self.lib.oracle_create(block_size, seed & 0xFFFFFFFFFFFFFFFF, policy)
         if not self.h:
             raise ValueError("oracle_create: bad arguments")
         self.capacity = capacity
+        self.components = components
+        if components != 1 and self.lib.oracle_set_components(self.h, components):
+            raise ValueError("components must be 1 or 2")
         if capacity:
             self.lib.oracle_set_capacity(self.h, capacity)   # LRU eviction (DESIGN.md R22-R25)
 
@@ -155,6 +162,22 @@ class Oracle:
 
     def sigma(self, user: int) -> int:
         return int(self.lib.oracle_sigma(self.h, user))
+
+    def params2(self):
+        B2, M2 = ctypes.c_uint64(), ctypes.c_uint64()
+        self.lib.oracle_params2(self.h, ctypes.byref(B2), ctypes.byref(M2))
+        return int(B2.value), int(M2.value)
+
+    def chain2(self, tokens, user: int = 0, divert_at: int = -1):
+        """(S, S2, keys) of both H-def components (keys per the context's component count)."""
+        tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+        n = tokens.size // self.block_size
+        S = np.zeros(max(n, 1), dtype=np.uint64)
+        S2 = np.zeros(max(n, 1), dtype=np.uint64)
+        K = np.zeros(max(n, 1), dtype=np.uint64)
+        self.lib.oracle_chain2(self.h, _ptr(tokens if tokens.size else np.zeros(1, np.uint32)),
+                               n, user, divert_at, _ptr(S), _ptr(S2), _ptr(K))
+        return S[:n], S2[:n], K[:n]
 
     def chain(self, tokens, user: int = 0, divert_at: int = -1):
         tokens = np.ascontiguousarray(tokens, dtype=np.uint32)

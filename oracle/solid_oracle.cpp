@@ -77,6 +77,11 @@ struct Ctx {
   int policy;        // 0 = APC, 1 = USER_ISOLATION, 2 = SOLIDARITY
   uint64_t B, M;
   std::vector<uint64_t> K;   // K_i = B^i mod p
+  // H-def v3 second component (SURVEY f4 hardening): an independent polynomial
+  // chain with base B2 and salts sigma2; the key then depends on both 61-bit chain values
+  int components;            // 1 (H-def v2) or 2
+  uint64_t B2, M2;
+  std::vector<uint64_t> K2;
   std::unordered_map<uint64_t, Entry> table;
   uint64_t next_seq;
   // LRU eviction (SPEC evict_lru S:117-125; R22-R25).  capacity 0 = unbounded (no
@@ -92,10 +97,30 @@ uint64_t sigma_of(const Ctx& c, uint32_t user) {
   return 1 + splitmix64(c.seed ^ SIGMA_SALT ^ (uint64_t)user) % (P61 - 1);
 }
 
+// second component (H-def v3): same construction with its own seed constants
+const uint64_t SEED2_SALT = 0xA0761D6478BD642FULL;
+const uint64_t SIGMA2_SALT = 0xE7037ED1A0B428DBULL;
+const uint64_t MIX2 = 0x9E3779B97F4A7C15ULL;
+uint64_t sigma2_of(const Ctx& c, uint32_t user) {
+  return 1 + splitmix64(c.seed ^ SIGMA2_SALT ^ (uint64_t)user) % (P61 - 1);
+}
+
+// key of a chain position: H-def v2 key_of(S) with one component; with two,
+// key = fmix64((S ^ (S2 * MIX2 mod 2^64)) + KEY_OFFSET), 0 -> 1
+uint64_t key2_of(uint64_t S, uint64_t S2) {
+  uint64_t k = fmix64((S ^ (S2 * MIX2)) + KEY_OFFSET);
+  return k == 0 ? 1 : k;
+}
+
 // h(block) = sum_i x_i * K_i mod p, x_i = token_i + 1
 uint64_t block_hash(const Ctx& c, const uint32_t* tok) {
   uint64_t h = 0;
   for (uint32_t i = 0; i < c.bs; ++i) h = addmod(h, mulmod((uint64_t)tok[i] + 1, c.K[i]));
+  return h;
+}
+uint64_t block_hash2(const Ctx& c, const uint32_t* tok) {
+  uint64_t h = 0;
+  for (uint32_t i = 0; i < c.bs; ++i) h = addmod(h, mulmod((uint64_t)tok[i] + 1, c.K2[i]));
   return h;
 }
 
@@ -173,6 +198,12 @@ void* oracle_create(uint32_t block_size, uint64_t seed, int policy) {
   uint64_t pw = 1;
   for (uint32_t i = 0; i < block_size; ++i) { c->K[i] = pw; pw = mulmod(pw, c->B); }
   c->M = pw;                  // M = B^bs
+  c->components = 1;
+  c->B2 = (1ULL << 32) + splitmix64(seed ^ SEED2_SALT) % (P61 - (1ULL << 33));
+  c->K2.resize(block_size);
+  pw = 1;
+  for (uint32_t i = 0; i < block_size; ++i) { c->K2[i] = pw; pw = mulmod(pw, c->B2); }
+  c->M2 = pw;
   c->next_seq = 0;
   c->capacity = 0;
   c->evictions = 0;
@@ -188,6 +219,20 @@ int oracle_set_capacity(void* h, uint64_t capacity) {
 }
 
 uint64_t oracle_evictions(void* h) { return ((Ctx*)h)->evictions; }
+
+// H-def components (1 or 2).  Must be set on an empty table.
+int oracle_set_components(void* h, int components) {
+  Ctx* c = (Ctx*)h;
+  if (!c->table.empty() || components < 1 || components > 2) return 1;
+  c->components = components;
+  return 0;
+}
+
+void oracle_params2(void* h, uint64_t* B2, uint64_t* M2) {
+  Ctx* c = (Ctx*)h;
+  *B2 = c->B2;
+  *M2 = c->M2;
+}
 uint64_t oracle_next_seq(void* h) { return ((Ctx*)h)->next_seq; }
 
 void oracle_destroy(void* h) { delete (Ctx*)h; }
@@ -207,19 +252,29 @@ uint64_t oracle_fmix64(uint64_t x) { return fmix64(x); }
 
 // Chain values and keys of one prompt of n_blocks full blocks: blocks 1..f are Shared, blocks
 // f+1..n in Iso(user) (f = -1 -> all Shared; f = 0 -> USER_ISOLATION chain from the root).
+void oracle_chain2(void* h, const uint32_t* tokens, uint32_t n_blocks, uint32_t user,
+                   int32_t divert_at, uint64_t* S_out, uint64_t* S2_out, uint64_t* keys_out) {
+  Ctx* c = (Ctx*)h;
+  uint64_t S = 0, Mp = 1, S2 = 0, Mp2 = 1;
+  const uint64_t sg = sigma_of(*c, user), sg2 = sigma2_of(*c, user);
+  for (uint32_t b = 1; b <= n_blocks; ++b) {
+    const uint32_t* blk = tokens + (uint64_t)(b - 1) * c->bs;
+    const bool iso = divert_at >= 0 && (int64_t)b > (int64_t)divert_at;
+    S = chain_step(S, Mp, block_hash(*c, blk), iso ? sg : 0);
+    Mp = mulmod(Mp, c->M);
+    S2 = chain_step(S2, Mp2, block_hash2(*c, blk), iso ? sg2 : 0);
+    Mp2 = mulmod(Mp2, c->M2);
+    if (S_out) S_out[b - 1] = S;
+    if (S2_out) S2_out[b - 1] = S2;
+    if (keys_out) keys_out[b - 1] = c->components == 2 ? key2_of(S, S2) : key_of(S);
+  }
+}
+
+// Chain values and keys of one prompt of n_blocks full blocks: blocks 1..f are Shared, blocks
+// f+1..n in Iso(user) (f = -1 -> all Shared; f = 0 -> USER_ISOLATION chain from the root).
 void oracle_chain(void* h, const uint32_t* tokens, uint32_t n_blocks, uint32_t user,
                   int32_t divert_at, uint64_t* S_out, uint64_t* keys_out) {
-  Ctx* c = (Ctx*)h;
-  uint64_t S = 0, Mp = 1;
-  const uint64_t sg = sigma_of(*c, user);
-  for (uint32_t b = 1; b <= n_blocks; ++b) {
-    uint64_t hb = block_hash(*c, tokens + (uint64_t)(b - 1) * c->bs);
-    uint64_t sigma = (divert_at >= 0 && (int64_t)b > (int64_t)divert_at) ? sg : 0;
-    S = chain_step(S, Mp, hb, sigma);
-    Mp = mulmod(Mp, c->M);
-    if (S_out) S_out[b - 1] = S;
-    if (keys_out) keys_out[b - 1] = key_of(S);
-  }
+  oracle_chain2(h, tokens, n_blocks, user, divert_at, S_out, nullptr, keys_out);
 }
 
 // Validate a whole batch first; no side effects on error.
@@ -243,7 +298,8 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
   Ctx& c = *(Ctx*)h;
   int err = oracle_validate(tokens, offsets, n_req, users);
   if (err) return err;
-  std::vector<uint64_t> hsh, S, Kk, I;
+  std::vector<uint64_t> hsh, hsh2, S, S2, Kk, I;
+  const bool two = c.components == 2;
   for (uint64_t j = 0; j < n_req; ++j, ++c.next_seq) {
     const uint32_t u = users[j];
     const bool e = enforce ? enforce[j] != 0 : true;
@@ -252,19 +308,26 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
     // hashed or cached ("block size of 16")
     hsh.assign(n + 1, 0);
     for (uint32_t b = 1; b <= n; ++b) hsh[b] = block_hash(c, tok + (uint64_t)(b - 1) * c.bs);
+    hsh2.assign(n + 1, 0);
+    if (two)
+      for (uint32_t b = 1; b <= n; ++b) hsh2[b] = block_hash2(c, tok + (uint64_t)(b - 1) * c.bs);
 
     uint32_t k = 0, r = 0, flagd = 0;
     int32_t f = -1;
 
     if (c.policy == 1) {
       // USER_ISOLATION baseline: a per-user namespace from the root.
-      const uint64_t sg = sigma_of(c, u);
+      const uint64_t sg = sigma_of(c, u), sg2 = sigma2_of(c, u);
       I.assign(n + 1, 0);
-      uint64_t T = 0, Mp = 1;
+      uint64_t T = 0, Mp = 1, T2 = 0, Mp2 = 1;
       for (uint32_t b = 1; b <= n; ++b) {
         T = chain_step(T, Mp, hsh[b], sg);
         Mp = mulmod(Mp, c.M);
-        I[b] = key_of(T);
+        if (two) {
+          T2 = chain_step(T2, Mp2, hsh2[b], sg2);
+          Mp2 = mulmod(Mp2, c.M2);
+        }
+        I[b] = two ? key2_of(T, T2) : key_of(T);
       }
       while (r < n && present(c, I[r + 1])) ++r;
       for (uint32_t b = 1; b <= r; ++b) touch(c, I[b], c.next_seq);
@@ -273,12 +336,17 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
     } else {
       // Shared chain S[b] and keys K[b]
       S.assign(n + 1, 0);
+      S2.assign(n + 1, 0);
       Kk.assign(n + 1, 0);
-      uint64_t Mp = 1;
+      uint64_t Mp = 1, Mp2 = 1;
       for (uint32_t b = 1; b <= n; ++b) {
         S[b] = chain_step(S[b - 1], Mp, hsh[b], 0);
         Mp = mulmod(Mp, c.M);
-        Kk[b] = key_of(S[b]);
+        if (two) {
+          S2[b] = chain_step(S2[b - 1], Mp2, hsh2[b], 0);
+          Mp2 = mulmod(Mp2, c.M2);
+        }
+        Kk[b] = two ? key2_of(S[b], S2[b]) : key_of(S[b]);
       }
       // APC lookup: longest present prefix ("partial hits, starting from the beginning of the
       // prompt"; SPEC lookup_longest_prefix S:99-107).
@@ -317,15 +385,22 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
           // Selective isolation: reuse stops at the flagged prefix f; the
           // remaining blocks continue in the requester's isolated namespace rooted at S[f]
           // (R3): the chain is re-derived step by step with sigma(Iso(u)).
-          const uint64_t sg = sigma_of(c, u);
+          const uint64_t sg = sigma_of(c, u), sg2 = sigma2_of(c, u);
           I.assign(n + 1, 0);
-          uint64_t T = S[f];
-          uint64_t Mpf = 1;
-          for (uint32_t b = 1; b <= (uint32_t)f; ++b) Mpf = mulmod(Mpf, c.M);   // M^f
+          uint64_t T = S[f], T2 = S2[f];
+          uint64_t Mpf = 1, Mpf2 = 1;
+          for (uint32_t b = 1; b <= (uint32_t)f; ++b) {   // M^f (per component)
+            Mpf = mulmod(Mpf, c.M);
+            Mpf2 = mulmod(Mpf2, c.M2);
+          }
           for (uint32_t b = (uint32_t)f + 1; b <= n; ++b) {
             T = chain_step(T, Mpf, hsh[b], sg);
             Mpf = mulmod(Mpf, c.M);
-            I[b] = key_of(T);
+            if (two) {
+              T2 = chain_step(T2, Mpf2, hsh2[b], sg2);
+              Mpf2 = mulmod(Mpf2, c.M2);
+            }
+            I[b] = two ? key2_of(T, T2) : key_of(T);
           }
           uint32_t m = 0;
           while ((uint32_t)f + m < n && present(c, I[(uint32_t)f + m + 1])) ++m;
@@ -394,6 +469,7 @@ void oracle_copy_table(void* dst, void* src) {
   d->capacity = s->capacity;
   d->evictions = s->evictions;
   d->next_seq = s->next_seq;
+  d->components = s->components;
 }
 
 void oracle_reserve(void* h, uint64_t n) { ((Ctx*)h)->table.reserve(n); }
