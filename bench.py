@@ -318,6 +318,34 @@ def measure_policy_eval(dev, args):
                    "samples completed before each batch; synthetic TTFT stand-in)"}
 
 
+def measure_hash2(dev, args, d, stream_np):
+    """the same C2 step with H-def v3 two-component keys (hash_components=2,
+    DESIGN.md §11) — the ALU price of the hardening on the fused hash kernel."""
+    import torch
+    import paper_2603_10726_b200 as P
+    N, nblk = stream_np.n_requests, stream_np.n_blocks()
+    idx = P.Index("solidarity", capacity_blocks=max(nblk // 6, 1 << 20),
+                  max_batch_tokens=stream_np.n_tokens + 64, max_batch_requests=N, seed=SEED,
+                  device=dev.index or 0, hash_components=2)
+    out = torch.empty((N, 6), dtype=torch.int32, device=dev)
+    cs = torch.cuda.current_stream(dev)
+    ms, hk = [], []
+    for k in range(args.warmup + max(args.steps, 3)):
+        idx.reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        idx.admit_async(d["tokens"], d["offsets"], d["users"], d["enforce"], out=out)
+        e1.record(cs)
+        idx.status()
+        if k >= args.warmup:
+            ms.append(e0.elapsed_time(e1))
+            hk.append(idx.stats()["ms_hash_kernel"])
+    med = statistics.median(ms)
+    return {"ms_per_step": med, "requests_per_s": N / (med / 1e3),
+            "hash_kernel_ms": statistics.median(hk),
+            "workload": "C2 bench batch (same inputs), hash_components=2"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -627,6 +655,10 @@ def main():
     if rank == 0 and world == 1 and not args.profile and not args.no_activator:
         activator = measure_activator(dev, args)
 
+    hash2 = None
+    if rank == 0 and world == 1 and not args.profile:
+        hash2 = measure_hash2(dev, args, d, stream_np)
+
     lru = None
     if rank == 0 and world == 1 and not args.profile and not args.no_evict:
         lru = measure_evict(dev, args)
@@ -660,6 +692,7 @@ def main():
             "cpu_baseline": cpu,
             "activator": activator,
             "lru_eviction": lru,
+            "hash_components_2": hash2,
             "policy_eval": peval,
             "e2e": e2e,
             "gpu_launches": int(sum(launches)),

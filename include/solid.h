@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SOLID_ABI_VERSION 3u
+#define SOLID_ABI_VERSION 4u
 #define SOLID_USER_NONE 0xFFFFFFFFu   /* "no user": sharer of an unflagged entry */
 
 typedef enum {
@@ -68,7 +68,12 @@ typedef struct {
                                   sequence number of the last request served it or inserted it
                                   (R22-R25).  Single GPU only (world == 1); capacity_blocks >=
                                   max_blocks.                                                     */
-  uint32_t reserved;           /* 0                                                              */
+  uint32_t hash_components;    /* 0 or 1: H-def v2 keys (one 61-bit polynomial chain).  2: H-def
+                                  v3: a second independent chain (base
+                                  B2) mixed into every key — the chain collision bound drops from
+                                  ~L/2^61 to ~L^2/2^122 per pair (L = tokens), below the 64-bit
+                                  key's 2^-64.  Decisions are unchanged (absent collisions); keys
+                                  differ.  world == 1 only.                                       */
 } solid_config;
 
 typedef struct solid_ctx solid_ctx;

@@ -52,7 +52,7 @@ class _Config(ctypes.Structure):
                 ("max_batch_requests", ctypes.c_uint64), ("hash_seed", ctypes.c_uint64),
                 ("policy", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32),
-                ("evict", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("evict", ctypes.c_uint32), ("hash_components", ctypes.c_uint32)]
 
 
 class _Batch(ctypes.Structure):
@@ -168,13 +168,14 @@ class Index:
     def __init__(self, policy: str = "solidarity", capacity_blocks: int = 1 << 20,
                  max_batch_tokens: int = 1 << 24, max_batch_requests: int = 1 << 16,
                  max_blocks: int = 8192, seed: int = 0x5011D000, device: int = 0,
-                 world: int = 1, rank: int = 0, evict: bool = False):
+                 world: int = 1, rank: int = 0, evict: bool = False, hash_components: int = 1):
         """evict=True: LRU eviction at capacity_blocks instead of
-        SOLID_ERR_CAPACITY; lookup() then synchronises its stream."""
+        SOLID_ERR_CAPACITY; lookup() then synchronises its stream.  hash_components=2: H-def v3
+        two-component keys."""
         self.lib = load_library()
         cfg = _Config(16, max_blocks, capacity_blocks, max_batch_tokens, max_batch_requests,
                       seed & 0xFFFFFFFFFFFFFFFF, POLICY[policy], device, world, rank,
-                      1 if evict else 0, 0)
+                      1 if evict else 0, hash_components)
         self.world, self.rank = world, rank
         h = ctypes.c_void_p()
         rc = self.lib.solid_init(ctypes.byref(cfg), ctypes.byref(h))

@@ -85,6 +85,13 @@ struct KParams {
   unsigned long long ksum_lo, ksum_hi;   // sum_i K_lo, sum_i K_hi (the "+1" of x = token + 1)
   const unsigned long long* mpow;  // M^i, i < max_blocks
   const unsigned long long* gtab;  // G[d] = sum_{t<d} M^t, d <= max_blocks
+  // H-def v3 second component (nc == 2): same layout for base B2
+  int nc;
+  uint32_t klo2[kBS], khi2[kBS];
+  unsigned long long ksum_lo2, ksum_hi2;
+  const unsigned long long* mpow2;
+  const unsigned long long* gtab2;
+  ulonglong2* cs;                  // nc == 2: per key id, its chain values {S, S2}
   uint64_t seed;
   const uint32_t* tokens;
   const uint64_t* offsets;
@@ -279,7 +286,9 @@ __device__ __forceinline__ bool init_id_at(const KParams& kp, uint32_t id, uint6
   return present;
 }
 
-__device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key) {
+__device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key, uint64_t s1 = 0,
+                        uint64_t s2 = 0) {
+  if (kp.nc == 2) kp.cs[id] = make_ulonglong2(s1, s2);   // published with the id (below)
   uint32_t owner = kNone, sharer = kNone;
   uint64_t ipos = 0;
   // sharded mode: a local table entry may belong to another shard; its state comes from there
@@ -292,7 +301,8 @@ __device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key) {
 // allocated with one atomic per warp and probe step (segment `seg`).
 __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool active, uint64_t key,
                                                      uint32_t seg, int lane, bool& created,
-                                                     bool* snap_present = nullptr) {
+                                                     bool* snap_present = nullptr,
+                                                     uint64_t s1 = 0, uint64_t s2 = 0) {
   const unsigned long long kx = key ^ kp.salt;
   const uint32_t E = kp.epoch;
   uint64_t pos = scratch_home(key, kp.smask);
@@ -344,7 +354,7 @@ __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool act
             id = mine;
             created = true;
             done = true;
-            const bool pr = init_id(kp, id, key);
+            const bool pr = init_id(kp, id, key, s1, s2);
             if (snap_present) *snap_present = pr;
           } else {
             e = old;                                // authoritative current value: re-examine
@@ -420,17 +430,30 @@ struct BlockWords {
     // lo + hi*2^32 mod p, with hi*2^32 = (hi mod 2^29)*2^32 + (hi >> 29)*2^61 == ... + (hi >> 29)
     return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
   }
+  // second component (base B2), same limb scheme
+  __device__ __forceinline__ uint64_t hash2(const KParams& kp) const {
+    uint64_t lo = kp.ksum_lo2, hi = kp.ksum_hi2;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t t = w[i + SH];
+      lo += (uint64_t)t * kp.klo2[i];
+      hi += (uint64_t)t * kp.khi2[i];
+    }
+    return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
+  }
 };
 
-template <int POLICY, int SH>
+template <int POLICY, int SH, int NC>
 __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uint64_t j, int lane,
                                                           const uint32_t* base, uint32_t n,
                                                           uint64_t blk0, uint32_t u,
                                                           uint32_t seg) {
   const uint64_t sig = (POLICY == SOLID_POLICY_USER_ISOLATION) ? sigma_of(kp.seed, u) : 0;
+  const uint64_t sig2 =
+      (NC == 2 && POLICY == SOLID_POLICY_USER_ISOLATION) ? sigma2_of(kp.seed, u) : 0;
   const unsigned long long guess =
       ((unsigned long long)tag_of(kp.epoch, 0) << 32) | (unsigned long long)(kp.seq_base + j + 1);
-  uint64_t carry = 0;
+  uint64_t carry = 0, carry2 = 0;
   uint32_t bad = 0;
   BlockWords<SH> cur, nxt;
   if ((uint32_t)lane < n) cur.load(base + (uint64_t)kBS * lane);
@@ -438,12 +461,21 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
     const uint32_t i = g + lane;
     const bool valid = i < n;
     if (i + 32 < n) nxt.load(base + (uint64_t)kBS * (i + 32));       // prefetch next group
-    uint64_t term = 0;
-    if (valid) term = mulmod(addmod(cur.hash(kp, bad), sig), kp.mpow[i]);
+    uint64_t term = 0, term2 = 0;
+    if (valid) {
+      term = mulmod(addmod(cur.hash(kp, bad), sig), kp.mpow[i]);
+      if (NC == 2) term2 = mulmod(addmod(cur.hash2(kp), sig2), kp.mpow2[i]);
+    }
     const uint64_t S = addmod(warp_scan_addmod(term, lane), carry);
     carry = __shfl_sync(0xffffffffu, S, 31);
+    uint64_t S2 = 0;
+    if (NC == 2) {
+      S2 = addmod(warp_scan_addmod(term2, lane), carry2);
+      carry2 = __shfl_sync(0xffffffffu, S2, 31);
+    }
     bool created = false;
-    const uint32_t id = scratch_register(kp, valid, key_of(S), seg, lane, created);
+    const uint32_t id = scratch_register(kp, valid, NC == 2 ? key2_of(S, S2) : key_of(S), seg,
+                                         lane, created, nullptr, S, S2);
     if (valid && id) {
       kp.id_of_block[blk0 + i] = id;
       // Round-0 state: the exact first occurrence (seq-min over all occurrences).  APC and
@@ -457,7 +489,7 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
   return bad;
 }
 
-template <int POLICY>
+template <int POLICY, int NC>
 __global__ void __launch_bounds__(256, 4) k_hash_register(KParams kp) {
   const int lane = threadIdx.x & 31;
   const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -484,23 +516,28 @@ __global__ void __launch_bounds__(256, 4) k_hash_register(KParams kp) {
   const uint32_t* base = kp.tokens + o0;
   uint32_t bad;
   switch (((uintptr_t)base >> 2) & 3) {
-    case 0: bad = hash_register_request<POLICY, 0>(kp, j, lane, base, n, blk0, u, seg); break;
-    case 1: bad = hash_register_request<POLICY, 1>(kp, j, lane, base, n, blk0, u, seg); break;
-    case 2: bad = hash_register_request<POLICY, 2>(kp, j, lane, base, n, blk0, u, seg); break;
-    default: bad = hash_register_request<POLICY, 3>(kp, j, lane, base, n, blk0, u, seg); break;
+    case 0: bad = hash_register_request<POLICY, 0, NC>(kp, j, lane, base, n, blk0, u, seg); break;
+    case 1: bad = hash_register_request<POLICY, 1, NC>(kp, j, lane, base, n, blk0, u, seg); break;
+    case 2: bad = hash_register_request<POLICY, 2, NC>(kp, j, lane, base, n, blk0, u, seg); break;
+    default: bad = hash_register_request<POLICY, 3, NC>(kp, j, lane, base, n, blk0, u, seg); break;
   }
   if (__any_sync(0xffffffffu, bad != 0) && lane == 0) set_err(kp.st, ERR_TOKEN);
 }
 
 // K_A on stream s (single GPU and sharded paths).
+template <int NC>
+static void launch_hash_nc(const KParams& kp, unsigned grid, cudaStream_t s) {
+  switch (kp.policy) {
+    case SOLID_POLICY_APC: k_hash_register<SOLID_POLICY_APC, NC><<<grid, 256, 0, s>>>(kp); break;
+    case SOLID_POLICY_USER_ISOLATION:
+      k_hash_register<SOLID_POLICY_USER_ISOLATION, NC><<<grid, 256, 0, s>>>(kp); break;
+    default: k_hash_register<SOLID_POLICY_SOLIDARITY, NC><<<grid, 256, 0, s>>>(kp); break;
+  }
+}
 static cudaError_t launch_hash(const KParams& kp, cudaStream_t s) {
   const unsigned grid = (unsigned)((kp.n * 32 + 255) / 256);
-  switch (kp.policy) {
-    case SOLID_POLICY_APC: k_hash_register<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(kp); break;
-    case SOLID_POLICY_USER_ISOLATION:
-      k_hash_register<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(kp); break;
-    default: k_hash_register<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(kp); break;
-  }
+  if (kp.nc == 2) launch_hash_nc<2>(kp, grid, s);
+  else launch_hash_nc<1>(kp, grid, s);
   return cudaGetLastError();
 }
 
@@ -513,9 +550,16 @@ __device__ __forceinline__ uint32_t owner_from(const KParams& kp, uint32_t id, u
 }
 
 __device__ __forceinline__ uint64_t iso_key(const KParams& kp, uint64_t blk, uint32_t i,
-                                            uint64_t sig, uint64_t gf) {
-  const uint64_t S = chain_of(kp.cold[kp.id_of_block[blk]].key);
+                                            uint64_t sig, uint64_t gf, uint64_t sig2 = 0,
+                                            uint64_t gf2 = 0) {
+  const uint32_t sid = kp.id_of_block[blk];
   const uint64_t d = submod(kp.gtab[i + 1], gf);   // G[b] - G[f], b = i + 1
+  if (kp.nc == 2) {   // chain values stored at registration (a 64-bit key cannot hold both)
+    const ulonglong2 c = kp.cs[sid];
+    const uint64_t d2 = submod(kp.gtab2[i + 1], gf2);
+    return key2_of(addmod(c.x, mulmod(sig, d)), addmod(c.y, mulmod(sig2, d2)));
+  }
+  const uint64_t S = chain_of(kp.cold[sid].key);
   return key_of(addmod(S, mulmod(sig, d)));
 }
 
@@ -648,12 +692,14 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
       // present in the index snapshot
       const uint64_t sig = sigma_of(kp.seed, u);
       const uint64_t gf = kp.gtab[f];
+      const uint64_t sig2 = kp.nc == 2 ? sigma2_of(kp.seed, u) : 0;
+      const uint64_t gf2 = kp.nc == 2 ? kp.gtab2[f] : 0;
       bool found = false;
       for (uint32_t g = (uint32_t)f; g < n; g += 32) {
         const uint32_t i = g + lane;
         const bool valid = i < n;
         uint64_t key = 0;
-        if (valid) key = iso_key(kp, blk0 + i, i, sig, gf);
+        if (valid) key = iso_key(kp, blk0 + i, i, sig, gf, sig2, gf2);
         bool created, snap = false;
         const uint32_t id = scratch_register(kp, valid, key, seg, lane, created, &snap);
         bool bvis = false;
@@ -1015,6 +1061,12 @@ struct solid_ctx {
   unsigned long long* mpow = nullptr;
   unsigned long long* gtab = nullptr;
   uint32_t klo[kBS], khi[kBS];
+  // H-def v3 second component (hash_components == 2)
+  int nc = 1;
+  unsigned long long* mpow2 = nullptr;
+  unsigned long long* gtab2 = nullptr;
+  ulonglong2* cs = nullptr;
+  uint32_t klo2[kBS], khi2[kBS];
   uint32_t epoch = 0;
   // pending batch
   KParams kp{};
@@ -1102,6 +1154,9 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->live_dev);
   cudaFree(c->mpow);
   cudaFree(c->gtab);
+  cudaFree(c->mpow2);
+  cudaFree(c->gtab2);
+  cudaFree(c->cs);
   cudaFree(c->h_tokens);
   cudaFree(c->h_offsets);
   cudaFree(c->h_users);
@@ -1141,6 +1196,8 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   const uint32_t world = cfg->world ? cfg->world : 1;
   if (world > 64 || cfg->rank >= world) return SOLID_ERR_INVALID;
   if (cfg->evict > 1 || (cfg->evict && (world != 1 || cfg->capacity_blocks < cfg->max_blocks)))
+    return SOLID_ERR_INVALID;
+  if (cfg->hash_components > 2 || (cfg->hash_components == 2 && world != 1))
     return SOLID_ERR_INVALID;
   ctx = new solid_ctx();
   ctx->cfg = *cfg;
@@ -1199,6 +1256,29 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   }
   CK(cudaMemcpy(ctx->mpow, mp.data(), mb * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->gtab, g.data(), (mb + 1) * 8, cudaMemcpyHostToDevice));
+  if (cfg->hash_components == 2) {   // H-def v3 second component: base B2, its own tables
+    ctx->nc = 2;
+    const uint64_t B2 = (1ull << 32) + splitmix64(cfg->hash_seed ^ kSeed2Salt) % (kP - (1ull << 33));
+    uint64_t p2 = 1;
+    for (uint32_t i = 0; i < kBS; ++i) {
+      ctx->klo2[i] = (uint32_t)p2;
+      ctx->khi2[i] = (uint32_t)(p2 >> 32);
+      p2 = mulmod_host(p2, B2);
+    }
+    const uint64_t M2 = p2;
+    uint64_t y = 1;
+    g[0] = 0;
+    for (uint64_t i = 0; i < mb; ++i) {
+      mp[i] = y;
+      g[i + 1] = addmod(g[i], y);
+      y = mulmod_host(y, M2);
+    }
+    CK(cudaMalloc(&ctx->mpow2, mb * 8));
+    CK(cudaMalloc(&ctx->gtab2, (mb + 1) * 8));
+    CK(cudaMalloc(&ctx->cs, ctx->idcap * sizeof(ulonglong2)));
+    CK(cudaMemcpy(ctx->mpow2, mp.data(), mb * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->gtab2, g.data(), (mb + 1) * 8, cudaMemcpyHostToDevice));
+  }
   CK(cudaMemset(ctx->tab, 0, ctx->tcap * sizeof(ulonglong2)));
   solid_status rc = init_scratch(ctx, 0);
   if (rc != SOLID_OK) return rc;
@@ -1298,6 +1378,17 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   kp.mpow = ctx->mpow;
   kp.gtab = ctx->gtab;
   kp.seed = ctx->cfg.hash_seed;
+  kp.nc = ctx->nc;
+  memcpy(kp.klo2, ctx->klo2, sizeof(kp.klo2));
+  memcpy(kp.khi2, ctx->khi2, sizeof(kp.khi2));
+  kp.ksum_lo2 = kp.ksum_hi2 = 0;
+  for (uint32_t i = 0; i < kBS && ctx->nc == 2; ++i) {
+    kp.ksum_lo2 += ctx->klo2[i];
+    kp.ksum_hi2 += ctx->khi2[i];
+  }
+  kp.mpow2 = ctx->mpow2;
+  kp.gtab2 = ctx->gtab2;
+  kp.cs = ctx->cs;
   kp.tokens = b->tokens;
   kp.offsets = b->offsets;
   kp.users = b->users;

@@ -80,6 +80,19 @@ __host__ __device__ __forceinline__ uint64_t sigma_of(uint64_t seed, uint32_t us
   return 1 + splitmix64(seed ^ kSigmaSalt ^ (uint64_t)user) % (kP - 1);
 }
 
+// H-def v3: second component — its own base seed and salts; the key mixes both
+// 61-bit chain values before the finaliser.
+constexpr uint64_t kSeed2Salt = 0xA0761D6478BD642Full;
+constexpr uint64_t kSigma2Salt = 0xE7037ED1A0B428DBull;
+constexpr uint64_t kMix2 = 0x9E3779B97F4A7C15ull;
+__host__ __device__ __forceinline__ uint64_t sigma2_of(uint64_t seed, uint32_t user) {
+  return 1 + splitmix64(seed ^ kSigma2Salt ^ (uint64_t)user) % (kP - 1);
+}
+__host__ __device__ __forceinline__ uint64_t key2_of(uint64_t S, uint64_t S2) {
+  uint64_t k = fmix64((S ^ (S2 * kMix2)) + kKeyOffset);
+  return k ? k : 1;
+}
+
 // Inclusive warp scan of values in [0, p) under addition mod p.
 __device__ __forceinline__ uint64_t warp_scan_addmod(uint64_t x, int lane) {
 #pragma unroll
