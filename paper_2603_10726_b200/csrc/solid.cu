@@ -1204,7 +1204,8 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   ctx->cfg.world = world;
   ctx->dev = cfg->device;
   CK(cudaSetDevice(ctx->dev));
-  ctx->tcap = next_pow2(std::max<uint64_t>(2 * cfg->capacity_blocks, 1024));
+  // evict mode: 4x headroom so the tombstones of ~C/4 evictions fit between rebuilds
+  ctx->tcap = next_pow2(std::max<uint64_t>((cfg->evict ? 4 : 2) * cfg->capacity_blocks, 1024));
   ctx->slot_cap = cfg->max_batch_tokens / kBS + 1;
   // distinct keys per batch <= Shared keys + isolated keys of every divert depth tried; ids are
   // allocated from kNSeg segments chosen by request, each with 2x headroom over an even share
