@@ -16,7 +16,11 @@
 //  attacker experiment (golden/p2_attack.json), the §5 guarantee by brute force
 //  (P:560-603), APC == brute-force longest common prefix, user isolation == per-user LCP,
 //  enforce=0 == APC, an independent content-keyed trie reference, splitmix64 published vector,
-//  and the chain value against a closed-form big-integer polynomial.
+//  and the chain value against a closed-form big-integer polynomial.  LRU eviction (capacity > 0,
+//  SPEC evict_lru S:117-125): the SPEC examples, Mattson's stack-distance theorem, the cyclic
+//  thrash closed form, a brute-force trie LRU (tests/test_oracle_eviction.py).  Two-component keys
+//  (H-def v3): both chains against their closed forms, exhaustive no-collision, decision
+//  invariance (tests/test_oracle_hash2.py).
 //  "parity unpinned": fmix64 outputs (an arbitrary finaliser; pinned only by bijectivity and by
 //  agreement with the independent CUDA implementation).
 // ============================================================================================
