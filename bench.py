@@ -299,6 +299,29 @@ def measure_policy_eval(dev, args):
                                       for i in range(0, s.n_requests, 100)])
                 row[pol] = round(hit_rate(res), 4)
             table[f"{gname}:{w}"] = row
+    # the same workloads under cache pressure: LRU eviction (evict mode) at 1000 entries, about a
+    # third of the smallest working set (cf. the paper's LLaMA-13B remark)
+    def admit_lru(policy, s, cap=1000, batch=25):
+        idx = P.Index(policy, capacity_blocks=cap, max_batch_tokens=s.n_tokens + 64,
+                      max_batch_requests=batch, max_blocks=64, seed=SEED, device=dev.index or 0,
+                      evict=True)
+
+        def one(b):
+            try:
+                return P.as_numpy(idx.admit(**P.to_device(b, dev)))
+            except P.SolidError as e:
+                if e.status != P.SOLID_ERR_CAPACITY or b.n_requests < 2:
+                    raise
+                h = b.n_requests // 2
+                return np.concatenate([one(b.slice(0, h)), one(b.slice(h, b.n_requests))])
+        return np.concatenate([one(s.slice(i, min(i + batch, s.n_requests)))
+                               for i in range(0, s.n_requests, batch)])
+    table_lru = {}
+    for gname, gen in (("single", preset), ("two_level", two_level)):
+        for w in PRESETS:
+            s = gen(w)
+            table_lru[f"{gname}:{w}"] = {pol: round(hit_rate(admit_lru(pol, s)), 4)
+                                         for pol in ("apc", "user_isolation", "solidarity")}
     s = two_level("W4")
     d = lambda a, t: torch.from_numpy(np.ascontiguousarray(a)).to(dtype=t, device=dev)
     sweep = {}
@@ -312,7 +335,8 @@ def measure_policy_eval(dev, args):
                               "enforced": round(float(en.mean()), 3)}
     return {"workloads": "W1-W5 presets (10 users x 100 requests, seed 0x5011D0F3); two_level = "
                          "templates in families of 8 sharing a 3-block preamble",
-            "hit_rates": table, "theta_sweep_two_level_W4": sweep,
+            "hit_rates": table, "hit_rates_lru_1000_entries": table_lru,
+            "theta_sweep_two_level_W4": sweep,
             "wall_s": time.perf_counter() - t0,
             "how": "library admission in batches of 100 (sweep: 50, Activator windows of the "
                    "samples completed before each batch; synthetic TTFT stand-in)"}

@@ -77,3 +77,29 @@ def test_theta_sweep_closed_loop(theta):
     assert np.array_equal(np.isnan(ov_g), np.isnan(ov_o))
     assert np.abs(ov_g[ok] - ov_o[ok]).max() <= 1e-9
     assert 0.0 <= hit_rate(res) <= 1.0
+
+
+@pytest.mark.parametrize("w", ["W3", "W5"])
+@pytest.mark.parametrize("policy", ["apc", "user_isolation", "solidarity"])
+def test_workload_parity_under_lru_pressure(w, policy):
+    """The policy evaluation under a 1000-entry LRU cap (evict mode) matches the LRU oracle."""
+    import torch
+    import paper_2603_10726_b200 as P
+    s = two_level(w)
+    idx = P.Index(policy, capacity_blocks=1000, max_batch_tokens=s.n_tokens + 64,
+                  max_batch_requests=25, max_blocks=64, seed=SEED, evict=True)
+
+    def one(b):
+        try:
+            return P.as_numpy(idx.admit(**P.to_device(b)))
+        except P.SolidError as e:
+            assert e.status == P.SOLID_ERR_CAPACITY and b.n_requests > 1
+            h = b.n_requests // 2
+            return np.concatenate([one(b.slice(0, h)), one(b.slice(h, b.n_requests))])
+    got = np.concatenate([one(s.slice(i, min(i + 25, s.n_requests)))
+                          for i in range(0, s.n_requests, 25)])
+    torch.cuda.synchronize()
+    o = Oracle(16, SEED, POL[policy], capacity=1000)
+    assert np.array_equal(got, o.process(s))
+    gd, ed = idx.dump_ex(), o.dump_ex()
+    assert all(np.array_equal(gd[f], ed[f]) for f in ["key", "owner", "sharer", "last_used"])
