@@ -155,3 +155,32 @@ def test_checkpoint_restore_evict():
     r2 = _admit_split(idx, b, [])
     torch.cuda.synchronize()
     assert np.array_equal(r1, r2) and np.array_equal(d1, idx.dump_ex())
+
+
+def test_bench_configuration_full_size():
+    """bench.py's lru_eviction measurement exactly (C3 shape, 10 000 users, 1 M-entry LRU cap,
+    warm until full in 2 000-request batches, then the timed 2 000-request batch): every result
+    of the timed batch and the final index (incl. last_used) equal the LRU oracle's."""
+    import torch
+    import paper_2603_10726_b200 as P
+    cap, users, bsz = 1_000_000, 10_000, 2_000
+    warm, timed = c3_multiturn(users=users, warm_blocks=cap, timed_rounds=1, seed=SEED + 3)
+    batch = timed.slice(0, bsz)
+    wb = [warm.slice(i, min(i + bsz, warm.n_requests)) for i in range(0, warm.n_requests, bsz)]
+    idx = P.Index("solidarity", capacity_blocks=cap,
+                  max_batch_tokens=max(max(b.n_tokens for b in wb), batch.n_tokens) + 64,
+                  max_batch_requests=bsz, seed=SEED, evict=True)
+    for b in wb:
+        _admit_split(idx, b, [])
+    got = _admit_split(idx, batch, [])
+    torch.cuda.synchronize()
+    o = Oracle(16, SEED, 2, capacity=cap)
+    o.process(warm)
+    exp = o.process(batch)
+    for f in exp.dtype.names:
+        assert np.array_equal(got[f], exp[f]), f
+    gd, ed = idx.dump_ex(), o.dump_ex()
+    assert len(gd) == len(ed) == cap
+    for f in ["key", "owner", "sharer", "last_used"]:
+        assert np.array_equal(gd[f], ed[f]), f
+    assert idx.stats()["evicted"] == o.evictions()
