@@ -1136,6 +1136,7 @@ static solid_status evict_init(solid_ctx* ctx);
 static solid_status evict_lookup(solid_ctx* ctx, cudaStream_t s);
 static solid_status evict_insert(solid_ctx* ctx, cudaStream_t s);
 static solid_status evict_reset(solid_ctx* ctx, cudaStream_t s);
+static solid_status evict_scratch_reset(solid_ctx* ctx, cudaStream_t s);
 static solid_status evict_checkpoint(solid_ctx* ctx);
 static solid_status evict_restore(solid_ctx* ctx);
 
@@ -1175,6 +1176,10 @@ static solid_status init_scratch(solid_ctx* ctx, cudaStream_t s) {
                                   ctx->idcap * (sizeof(Hot) / 8), ~0ull);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
+  if (ctx->ev_state) {                       // id publication words carry the epoch
+    solid_status rc = evict_scratch_reset(ctx, s);
+    if (rc != SOLID_OK) return rc;
+  }
   ctx->epoch = 0;
   return SOLID_OK;
 }
