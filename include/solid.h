@@ -192,6 +192,19 @@ solid_status solid_batch_status(solid_ctx* ctx);
 solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* host_batch,
                               solid_result* out_host, void* stream);
 
+/* The same with 16-bit token ids (vocabularies up to 65 536 — Llama-2's 32 000, the paper's
+ * models): half the host->device bytes; the ids are widened on the device (k_widen16) before
+ * the admission.  Offsets, users and enforce as in solid_batch (HOST memory). */
+typedef struct {
+  uint64_t n_requests;
+  const uint16_t* tokens;
+  const uint64_t* offsets;
+  const uint32_t* users;
+  const uint8_t* enforce;
+} solid_batch_u16;
+solid_status solid_admit_host_u16(solid_ctx* ctx, const solid_batch_u16* host_batch,
+                                  solid_result* out_host, void* stream);
+
 solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out);
 
 /* Copy live entries to host_out (HOST memory, capacity `cap` entries) sorted by key; *n_out =

@@ -29,7 +29,7 @@ ENTRY_EX_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4"),
 
 # C ABI entry points declared in include/solid.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
-               "solid_insert_batch", "solid_admit_host", "solid_stats", "solid_dump", "solid_dump_ex",
+               "solid_insert_batch", "solid_admit_host", "solid_admit_host_u16", "solid_stats", "solid_dump", "solid_dump_ex",
                "solid_admit_batch", "solid_batch_status",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
@@ -117,6 +117,8 @@ def load_library(path: str = LIB_PATH):
     lib.solid_batch_status.argtypes = [vp]
     lib.solid_admit_host.restype = st
     lib.solid_admit_host.argtypes = [vp, ctypes.POINTER(_Batch), vp, vp]
+    lib.solid_admit_host_u16.restype = st
+    lib.solid_admit_host_u16.argtypes = [vp, ctypes.POINTER(_Batch), vp, vp]   # same layout
     lib.solid_stats.restype = st
     lib.solid_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
     lib.solid_dump.restype = st
@@ -274,6 +276,26 @@ class Index:
         self._check(self.lib.solid_admit_host(self.h, ctypes.byref(b),
                                               ctypes.c_void_p(out.ctypes.data),
                                               self._stream(stream)))
+        return out[:n]
+
+    def admit_host_u16(self, tokens: np.ndarray, offsets: np.ndarray, users: np.ndarray,
+                       enforce: Optional[np.ndarray] = None, out: Optional[np.ndarray] = None,
+                       stream=None) -> np.ndarray:
+        """admit_host with 16-bit token ids (solid_admit_host_u16): tokens must be uint16."""
+        if tokens.dtype != np.uint16 or not tokens.flags.c_contiguous:
+            raise ValueError("tokens must be a contiguous uint16 array")
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        users = np.ascontiguousarray(users, dtype=np.uint32)
+        en = None if enforce is None else np.ascontiguousarray(enforce, dtype=np.uint8)
+        n = users.shape[0]
+        if out is None:
+            out = np.zeros(max(n, 1), dtype=RESULT_DTYPE)
+        if tokens.size == 0:
+            tokens = np.zeros(8, np.uint16)
+        b = _Batch(n, _np_ptr(tokens), _np_ptr(offsets), _np_ptr(users), _np_ptr(en))
+        self._check(self.lib.solid_admit_host_u16(self.h, ctypes.byref(b),
+                                                  ctypes.c_void_p(out.ctypes.data),
+                                                  self._stream(stream)))
         return out[:n]
 
     # ---- inspection / state --------------------------------------------------------------

@@ -1022,6 +1022,7 @@ __global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long
 using namespace solid;
 
 constexpr uint32_t kRing = SOLID_MAX_INFLIGHT;   // asynchronous batches in flight per context
+constexpr uint32_t kHostChunks = 4;              // host admission: sub-batches of a large batch
 struct HostSlot {               // pinned host mirror of one batch's status
   DevStatus st;
 };
@@ -1075,6 +1076,10 @@ struct solid_ctx {
   cudaStream_t stream = nullptr;
   // host-buffer admission staging
   uint32_t* h_tokens = nullptr;
+  uint16_t* h_tokens16 = nullptr;
+  cudaStream_t s_copy = nullptr;               // host admission: token copies of later chunks
+  cudaEvent_t ev_chunk[kHostChunks + 1] = {};
+  uint64_t* h_offs_sub = nullptr;
   uint64_t* h_offsets = nullptr;
   uint32_t* h_users = nullptr;
   uint8_t* h_enforce = nullptr;
@@ -1159,6 +1164,11 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->gtab2);
   cudaFree(c->cs);
   cudaFree(c->h_tokens);
+  cudaFree(c->h_tokens16);
+  cudaFree(c->h_offs_sub);
+  for (auto& e : c->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  if (c->s_copy) cudaStreamDestroy(c->s_copy);
   cudaFree(c->h_offsets);
   cudaFree(c->h_users);
   cudaFree(c->h_enforce);
@@ -1609,16 +1619,47 @@ extern "C" solid_status solid_batch_status(solid_ctx* ctx) {
   return finish_batch(ctx, i, ctx->stream, true);
 }
 
-extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
-                                         solid_result* out_host, void* stream) {
+// 16-bit token ids widened to the library's 32-bit layout (8 tokens per thread, 16-byte loads
+// when the source is aligned).
+__global__ void __launch_bounds__(256) k_widen16(const uint16_t* in, uint32_t* out, uint64_t T) {
+  const uint64_t n8 = T / 8;
+  const bool al = ((uintptr_t)in & 15) == 0;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n8;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t w[4];
+    if (al) {
+      const uint4 v = reinterpret_cast<const uint4*>(in)[q];
+      w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    } else {
+      for (int k = 0; k < 4; ++k) w[k] = (uint32_t)in[8 * q + 2 * k] | ((uint32_t)in[8 * q + 2 * k + 1] << 16);
+    }
+    uint4 a = make_uint4(w[0] & 0xFFFFu, w[0] >> 16, w[1] & 0xFFFFu, w[1] >> 16);
+    uint4 b = make_uint4(w[2] & 0xFFFFu, w[2] >> 16, w[3] & 0xFFFFu, w[3] >> 16);
+    reinterpret_cast<uint4*>(out)[2 * q] = a;
+    reinterpret_cast<uint4*>(out)[2 * q + 1] = b;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (T & 7)) out[8 * n8 + threadIdx.x] = in[8 * n8 + threadIdx.x];
+}
+
+// offsets of a sub-batch rebased to 0
+__global__ void k_rebase(const uint64_t* in, uint64_t* out, uint64_t m) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = in[i] - in[0];
+}
+
+// Host-buffer admission: batch arrays copied in (tokens as 32- or 16-bit ids), lookup + insert,
+// results copied out; synchronises the stream.
+static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* tokens,
+                                      int token_bytes, const uint64_t* offsets,
+                                      const uint32_t* users, const uint8_t* enforce,
+                                      solid_result* out_host, void* stream) {
   if (!ctx) return SOLID_ERR_INVALID;
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
-  if (!hb || !hb->offsets || (hb->n_requests && (!hb->tokens || !hb->users || !out_host)))
+  if (!offsets || (n && (!tokens || !users || !out_host)))
     return fail(ctx, SOLID_ERR_INVALID, "null batch pointer");
-  const uint64_t n = hb->n_requests;
   if (n > ctx->cfg.max_batch_requests)
     return fail(ctx, SOLID_ERR_INVALID, "n_requests > max_batch_requests");
-  const uint64_t T = hb->offsets[n];
+  const uint64_t T = offsets[n];
   if (T > ctx->cfg.max_batch_tokens) return fail(ctx, SOLID_ERR_INVALID, "tokens > max_batch_tokens");
   CK(cudaSetDevice(ctx->dev));
   cudaStream_t s = (cudaStream_t)stream;
@@ -1630,23 +1671,81 @@ extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
     CK(cudaMalloc(&ctx->h_enforce, R + 1));
     CK(cudaMalloc(&ctx->h_out, R * sizeof(solid_result) + 32));
   }
-  if (T) CK(cudaMemcpyAsync(ctx->h_tokens, hb->tokens, T * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(ctx->h_offsets, hb->offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
-  if (n) CK(cudaMemcpyAsync(ctx->h_users, hb->users, n * 4, cudaMemcpyHostToDevice, s));
-  if (n && hb->enforce) CK(cudaMemcpyAsync(ctx->h_enforce, hb->enforce, n, cudaMemcpyHostToDevice, s));
-  solid_batch db;
-  db.n_requests = n;
-  db.tokens = ctx->h_tokens;
-  db.offsets = ctx->h_offsets;
-  db.users = ctx->h_users;
-  db.enforce = hb->enforce ? ctx->h_enforce : nullptr;
-  solid_status rc = solid_lookup_batch(ctx, &db, ctx->h_out, stream);
-  if (rc != SOLID_OK) return rc;
-  rc = solid_insert_batch(ctx, stream);
+  if (token_bytes == 2 && !ctx->h_tokens16)
+    CK(cudaMalloc(&ctx->h_tokens16, (ctx->cfg.max_batch_tokens + 8) * 2));
+  CK(cudaMemcpyAsync(ctx->h_offsets, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+  if (n) CK(cudaMemcpyAsync(ctx->h_users, users, n * 4, cudaMemcpyHostToDevice, s));
+  if (n && enforce) CK(cudaMemcpyAsync(ctx->h_enforce, enforce, n, cudaMemcpyHostToDevice, s));
+  // Large batches are admitted as kHostChunks consecutive sub-batches (identical results,
+  // reading R1) so the token copy of chunk k+1 (copy stream) overlaps the admission of chunk k.
+  const uint32_t K = (T * (uint64_t)token_bytes >= (64ull << 20) && n >= 4 * kHostChunks &&
+                      !ctx->ev_state) ? kHostChunks : 1u;
+  if (K > 1 && !ctx->s_copy) {
+    CK(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev_chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaMalloc(&ctx->h_offs_sub, (ctx->cfg.max_batch_requests + kHostChunks + 1) * 8));
+  }
+  cudaStream_t sc = K > 1 ? ctx->s_copy : s;
+  if (K > 1) {                       // the copy stream starts after the small copies were enqueued
+    CK(cudaEventRecord(ctx->ev_chunk[kHostChunks], s));
+    CK(cudaStreamWaitEvent(sc, ctx->ev_chunk[kHostChunks], 0));
+  }
+  for (uint32_t k = 0; k < K; ++k) {
+    const uint64_t a = offsets[n * k / K], b = offsets[n * (k + 1) / K];
+    if (b > a)
+      CK(cudaMemcpyAsync(token_bytes == 2 ? (void*)(ctx->h_tokens16 + a) : (void*)(ctx->h_tokens + a),
+                         (const char*)tokens + a * token_bytes, (b - a) * token_bytes,
+                         cudaMemcpyHostToDevice, sc));
+    if (K > 1) CK(cudaEventRecord(ctx->ev_chunk[k], sc));
+  }
+  solid_status rc = SOLID_OK;
+  for (uint32_t k = 0; k < K; ++k) {
+    const uint64_t lo = n * k / K, hi = n * (k + 1) / K;
+    const uint64_t a = offsets[lo], b = offsets[hi];
+    if (K > 1) CK(cudaStreamWaitEvent(s, ctx->ev_chunk[k], 0));
+    if (token_bytes == 2 && b > a) {   // widen from an 8-aligned start (earlier ids: same values)
+      const uint64_t a8 = a & ~7ull;
+      k_widen16<<<(unsigned)std::min<uint64_t>(((b - a8) / 8 + 255) / 256 + 1, 8192), 256, 0, s>>>(
+          ctx->h_tokens16 + a8, ctx->h_tokens + a8, b - a8);
+      CK(cudaGetLastError());
+    }
+    solid_batch db;
+    db.n_requests = hi - lo;
+    db.tokens = ctx->h_tokens + a;
+    if (K > 1) {
+      uint64_t* sub = ctx->h_offs_sub + lo + k;
+      k_rebase<<<(unsigned)((hi - lo + 1 + 255) / 256), 256, 0, s>>>(ctx->h_offsets + lo, sub,
+                                                                      hi - lo + 1);
+      CK(cudaGetLastError());
+      db.offsets = sub;
+    } else {
+      db.offsets = ctx->h_offsets;
+    }
+    db.users = ctx->h_users + lo;
+    db.enforce = enforce ? ctx->h_enforce + lo : nullptr;
+    rc = solid_lookup_batch(ctx, &db, ctx->h_out + lo, stream);
+    if (rc == SOLID_OK) rc = solid_insert_batch(ctx, stream);
+    if (rc != SOLID_OK) break;
+  }
+  if (K > 1) cudaStreamSynchronize(sc);       // no copy may outlive a failed call
   if (rc != SOLID_OK) return rc;
   if (n) CK(cudaMemcpyAsync(out_host, ctx->h_out, n * sizeof(solid_result), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return SOLID_OK;
+}
+
+extern "C" solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* hb,
+                                         solid_result* out_host, void* stream) {
+  if (!hb) return ctx ? fail(ctx, SOLID_ERR_INVALID, "null batch pointer") : SOLID_ERR_INVALID;
+  return admit_host_common(ctx, hb->n_requests, hb->tokens, 4, hb->offsets, hb->users,
+                           hb->enforce, out_host, stream);
+}
+
+extern "C" solid_status solid_admit_host_u16(solid_ctx* ctx, const solid_batch_u16* hb,
+                                             solid_result* out_host, void* stream) {
+  if (!hb) return ctx ? fail(ctx, SOLID_ERR_INVALID, "null batch pointer") : SOLID_ERR_INVALID;
+  return admit_host_common(ctx, hb->n_requests, hb->tokens, 2, hb->offsets, hb->users,
+                           hb->enforce, out_host, stream);
 }
 
 // Profiling build (-DSOLID_COUNTERS) only: the last collected batch's per-round path counters.

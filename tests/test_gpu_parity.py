@@ -252,6 +252,36 @@ def test_host_buffer_admission_matches():
     assert_same(got, exp, idx.dump(), ed, "admit_host")
 
 
+@pytest.mark.parametrize("name", ["c1", "c2_small", "random"])
+def test_host_buffer_admission_u16_matches(name):
+    """solid_admit_host_u16: 16-bit token ids widened on the device give the oracle's results
+    (ragged token counts, so the widening tail is exercised)."""
+    s = {"c1": c1_tiny, "c2_small": lambda: c2_shared_prompt(users=40, reqs_per_user=10),
+         "random": lambda: random_small(301, users=3, alphabet_blocks=4, max_blocks=6, seed=3)}[name]()
+    assert int(s.tokens.max()) < 65536
+    exp, ed = oracle_run(s, "solidarity")
+    idx = _index("solidarity", [s])
+    got = idx.admit_host_u16(s.tokens.astype(np.uint16), s.offsets, s.users, s.enforce)
+    assert_same(got, exp, idx.dump(), ed, "admit_host_u16")
+
+
+@pytest.mark.parametrize("u16", [False, True])
+def test_host_buffer_admission_chunked_pipeline(u16):
+    """Batches with >= 64 MB of token ids are admitted through the host path as 4 sub-batches
+    whose copies overlap the previous sub-batch's admission: same results and index as the
+    oracle (one stream, reading R1)."""
+    s = c2_shared_prompt(users=170, reqs_per_user=100)
+    assert s.n_tokens * (2 if u16 else 4) >= 64 << 20
+    exp, ed = oracle_run(s, "solidarity")
+    idx = _index("solidarity", [s])
+    if u16:
+        got = idx.admit_host_u16(s.tokens.astype(np.uint16), s.offsets, s.users, s.enforce)
+    else:
+        got = idx.admit_host(s.tokens, s.offsets, s.users, s.enforce)
+    assert_same(got, exp, idx.dump(), ed, "chunked admit_host")
+    assert idx.stats()["batches"] == 4
+
+
 def test_stats_are_consistent():
     s = c1_tiny()
     got, gd, idx = gpu_run(s, "solidarity")
