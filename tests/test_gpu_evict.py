@@ -184,3 +184,34 @@ def test_bench_configuration_full_size():
     for f in ["key", "owner", "sharer", "last_used"]:
         assert np.array_equal(gd[f], ed[f]), f
     assert idx.stats()["evicted"] == o.evictions()
+
+
+def test_empty_and_invalid_batches_leave_state_untouched():
+    """Evict mode: an empty batch and an invalid batch (token >= 2^20) change nothing — neither
+    the index (incl. last_used) nor the sequence clock — and later batches still match."""
+    import torch
+    import paper_2603_10726_b200 as P
+    s = random_small(200, users=3, alphabet_blocks=4, max_blocks=6, seed=8)
+    a, b = s.slice(0, 100), s.slice(100, 200)
+    idx = P.Index("solidarity", capacity_blocks=12, max_batch_tokens=1 << 16,
+                  max_batch_requests=256, max_blocks=8, seed=SEED, evict=True)
+    o = Oracle(16, SEED, 2, capacity=12)
+    got = [_admit_split(idx, a, [])]
+    o.process(a)
+    before = idx.dump_ex()
+    empty = s.slice(0, 0)
+    d = P.to_device(empty)
+    idx.admit(**d)
+    bad = b.slice(0, 10)
+    bad.tokens = bad.tokens.copy()
+    bad.tokens[3] = 1 << 20
+    with pytest.raises(P.SolidError) as ei:
+        idx.admit(**P.to_device(bad))
+    assert ei.value.status == P.SOLID_ERR_INVALID
+    assert np.array_equal(idx.dump_ex(), before)
+    got.append(_admit_split(idx, b, []))
+    torch.cuda.synchronize()
+    exp = o.process(b)
+    assert np.array_equal(got[1], exp)
+    gd, ed = idx.dump_ex(), o.dump_ex()
+    assert all(np.array_equal(gd[f], ed[f]) for f in ["key", "owner", "sharer", "last_used"])
