@@ -766,7 +766,20 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
       const unsigned long long pk = ((unsigned long long)seqp << 32) | (unsigned long long)u;
       for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.int_ins[ids[i]], pk);
     } else {
-      for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.hot[ids[i]].v[2 * W], mine);
+      // same divert depth as last round: the ids of blocks f..f+31 are already in registers
+      // (iso_pre_id, lane l = block f + l), so the scatter needs no dependent id load there
+      const bool pre = POLICY == SOLID_POLICY_SOLIDARITY && f >= 1 && f == fprev;
+      for (uint32_t i0 = r; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        uint32_t id = 0;
+        if (pre && i0 < (uint32_t)f + 32) {
+          const uint32_t v = __shfl_sync(0xffffffffu, iso_pre_id, (i - (uint32_t)f) & 31);
+          if (i < n) id = i < (uint32_t)f + 32 ? v : ids[i];
+        } else if (i < n) {
+          id = ids[i];
+        }
+        if (i < n) atomicMin(&kp.hot[id].v[2 * W], mine);
+      }
     }
   }
 
