@@ -613,8 +613,10 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   bool carry_flag = false;    // flagged(index g-1) from the previous group
   bool walked = false;
   bool iso_pre_vis = false;
+  uint32_t idq[4];            // ids of the last walked 128 blocks (from wbase), kept for the scatter
+  uint32_t wbase = 0;
   for (uint32_t base = 0; base <= n && !walked; base += 128) {
-    uint32_t idq[4];
+    wbase = base;
     ulonglong2 pq[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -766,15 +768,25 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
       const unsigned long long pk = ((unsigned long long)seqp << 32) | (unsigned long long)u;
       for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.int_ins[ids[i]], pk);
     } else {
-      // same divert depth as last round: the ids of blocks f..f+31 are already in registers
-      // (iso_pre_id, lane l = block f + l), so the scatter needs no dependent id load there
+      // ids already in registers need no dependent load: a request diverting at an unchanged
+      // depth has blocks f..f+31 in iso_pre_id (lane l = block f + l); a Shared one has the
+      // last walked 128 blocks in idq (lane l of idq[q] = block wbase + 32 q + l)
       const bool pre = POLICY == SOLID_POLICY_SOLIDARITY && f >= 1 && f == fprev;
+      const bool shr = f < 0;
       for (uint32_t i0 = r; i0 < n; i0 += 32) {
         const uint32_t i = i0 + lane;
         uint32_t id = 0;
         if (pre && i0 < (uint32_t)f + 32) {
           const uint32_t v = __shfl_sync(0xffffffffu, iso_pre_id, (i - (uint32_t)f) & 31);
           if (i < n) id = i < (uint32_t)f + 32 ? v : ids[i];
+        } else if (shr && i0 >= wbase && i0 < wbase + 128) {
+          const uint32_t src = (i - wbase) & 31, q = (i - wbase) >> 5;
+          const uint32_t v0 = __shfl_sync(0xffffffffu, idq[0], src);
+          const uint32_t v1 = __shfl_sync(0xffffffffu, idq[1], src);
+          const uint32_t v2 = __shfl_sync(0xffffffffu, idq[2], src);
+          const uint32_t v3 = __shfl_sync(0xffffffffu, idq[3], src);
+          const uint32_t v = q == 0 ? v0 : q == 1 ? v1 : q == 2 ? v2 : v3;
+          if (i < n) id = i < wbase + 128 ? v : ids[i];
         } else if (i < n) {
           id = ids[i];
         }
