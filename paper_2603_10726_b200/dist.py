@@ -157,10 +157,13 @@ def loopback_admit(shards: List[ShardedIndex], local_batches, seq_bases):
 
 
 class TorchExchange:
-    """One shard per rank of a torch.distributed process group (NCCL for CUDA buffers)."""
+    """One shard per rank of a torch.distributed process group (NCCL for CUDA buffers).
 
-    def __init__(self, shard: ShardedIndex, group=None):
-        self.shard, self.group = shard, group
+    staging=True moves the records through host tensors (for a gloo group, whose point-to-point
+    ops take CPU tensors: several ranks sharing one GPU in tests)."""
+
+    def __init__(self, shard: ShardedIndex, group=None, staging: bool = False):
+        self.shard, self.group, self.staging = shard, group, staging
 
     def exchange(self, send_counts_list):
         """Counts by all_to_all_single, records by batched point-to-point (NCCL groups them;
@@ -170,11 +173,13 @@ class TorchExchange:
         sh = self.shard
         rank = dist.get_rank(self.group)
         send_counts = np.asarray(send_counts_list[0], dtype=np.int64)
-        sc = torch.tensor(send_counts, device=sh.send.device)
+        sc = torch.tensor(send_counts, device="cpu" if self.staging else sh.send.device)
         rc = torch.empty_like(sc)
         dist.all_to_all_single(rc, sc, group=self.group)
         recv_counts = rc.cpu().numpy()
-        ops = []
+        if self.staging and sh.send.is_cuda:
+            torch.cuda.synchronize()
+        ops, landing = [], []
         for p in range(sh.world):
             ns, nr = int(send_counts[p]), int(recv_counts[p])
             if p == rank:
@@ -182,12 +187,20 @@ class TorchExchange:
                     sh.recv_region(p, ns).copy_(sh.send_region(p, ns))
                 continue
             if ns:
-                ops.append(dist.P2POp(dist.isend, sh.send_region(p, ns), p, self.group))
+                src = sh.send_region(p, ns)
+                ops.append(dist.P2POp(dist.isend, src.cpu() if self.staging else src, p,
+                                      self.group))
             if nr:
-                ops.append(dist.P2POp(dist.irecv, sh.recv_region(p, nr), p, self.group))
+                dst = sh.recv_region(p, nr)
+                buf = torch.empty(dst.numel(), dtype=dst.dtype) if self.staging else dst
+                ops.append(dist.P2POp(dist.irecv, buf, p, self.group))
+                if self.staging:
+                    landing.append((dst, buf))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        for dst, buf in landing:
+            dst.copy_(buf)
         if sh.send.is_cuda:
             torch.cuda.synchronize()
         return [recv_counts]
@@ -195,7 +208,8 @@ class TorchExchange:
     def allreduce_max(self, xs):
         import torch
         import torch.distributed as dist
-        v = torch.tensor([max(xs)], dtype=torch.int64, device=self.shard.send.device)
+        v = torch.tensor([max(xs)], dtype=torch.int64,
+                         device="cpu" if self.staging else self.shard.send.device)
         dist.all_reduce(v, op=dist.ReduceOp.MAX, group=self.group)
         return int(v.item())
 
