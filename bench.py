@@ -427,7 +427,7 @@ def run_sharded(args, world, rank, local):
     shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
                          max_batch_tokens=s.n_tokens + 64, max_batch_requests=per, seed=SEED,
                          device=local)
-    ex = TorchExchange(shard)
+    ex = TorchExchange(shard, staging=os.environ.get("SOLID_DIST_BACKEND", "nccl") != "nccl")
     coll = {"s": 0.0}
 
     def timed_exchange(counts):
@@ -550,9 +550,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SOLID_DIST_BACKEND=gloo: ranks may share GPUs (records staged through host memory) — a
+    # functional check of the N > 1 path on a one-GPU box; the measured runs use NCCL
+    backend = os.environ.get("SOLID_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         return run_sharded(args, world, rank, local)
 
     stream_np, desc = _workload(args.config, rank)
