@@ -138,6 +138,8 @@ struct KParams {
   uint32_t* win_ev;                // seq' of the evicting request, kNone = not evicted
   unsigned long long* win_oflg;    // [w][2] old-incarnation flagger (tagged, ping-pong)
   uint32_t* win_tau;               // first request served the key (post-pass)
+  uint8_t* win_skip;               // k_window's skip flag per window index (0 at creation)
+  uint32_t* win_dense;             // [rank] = window index + 1 (0 = no window key of that rank)
   uint32_t* ins_cnt;               // per request: entries it inserts (final round)
   uint32_t* lt;                    // per id: last request served it (final)
 };
@@ -261,6 +263,8 @@ __device__ __forceinline__ bool init_id_at(const KParams& kp, uint32_t id, uint6
       kp.win_ev[w] = kNone;
       kp.win_oflg[2 * w] = ~0ull;
       kp.win_oflg[2 * w + 1] = ~0ull;
+      kp.win_skip[w] = 0;
+      kp.win_dense[rank] = w + 1;    // ranks are unique: the window in rank order, unsorted
       c.win = w;
     }
 #ifdef SOLID_EVDEBUG
