@@ -207,6 +207,17 @@ solid_status solid_admit_host_u16(solid_ctx* ctx, const solid_batch_u16* host_ba
 
 solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out);
 
+/* Block table of the last admitted batch (paged-KV integration; call after
+ * solid_insert_batch, or after solid_batch_status collected the last solid_admit_batch, and
+ * before the next lookup): for request j and its block b < n_j,
+ *   keys_out[offsets[j] / 16 + b] = the key of the index entry that holds that block's KV —
+ * the Shared key K[b] when the request stayed in the Shared namespace (served or inserted), the
+ * requester's isolated key I_f[b] for b >= f when it was diverted at f (R3), U[b] under
+ * USER_ISOLATION.  A paged-KV manager maps these keys to physical blocks.  keys_out: DEVICE
+ * memory, ceil(total tokens / 16) entries; positions no request's full block covers are not
+ * written.  Enqueued on `stream`.  Single-GPU contexts only. */
+solid_status solid_block_keys(solid_ctx* ctx, unsigned long long* keys_out, void* stream);
+
 /* Copy live entries to host_out (HOST memory, capacity `cap` entries) sorted by key; *n_out =
  * number of live entries (may exceed cap; then only cap are written). */
 solid_status solid_dump(solid_ctx* ctx, solid_entry* host_out, uint64_t cap, uint64_t* n_out);

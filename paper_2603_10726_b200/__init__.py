@@ -30,7 +30,7 @@ ENTRY_EX_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4"),
 # C ABI entry points declared in include/solid.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
                "solid_insert_batch", "solid_admit_host", "solid_admit_host_u16", "solid_stats", "solid_dump", "solid_dump_ex",
-               "solid_admit_batch", "solid_batch_status",
+               "solid_admit_batch", "solid_batch_status", "solid_block_keys",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
                "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit",
@@ -123,6 +123,8 @@ def load_library(path: str = LIB_PATH):
     lib.solid_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
     lib.solid_dump.restype = st
     lib.solid_dump.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+    lib.solid_block_keys.restype = st
+    lib.solid_block_keys.argtypes = [vp, vp, vp]
     lib.solid_dump_ex.restype = st
     lib.solid_dump_ex.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
     for name in ["solid_reset", "solid_checkpoint", "solid_restore"]:
@@ -313,6 +315,16 @@ class Index:
         self._check(self.lib.solid_dump(self.h, ctypes.c_void_p(out.ctypes.data), n.value,
                                         ctypes.byref(n)))
         return out[:int(n.value)]
+
+    def block_keys(self, n_tokens: int, stream=None):
+        """Block table of the last batch (solid_block_keys): uint64 tensor [ceil(T/16)], the key
+        of the entry holding each block's KV (index offsets[j] // 16 + b)."""
+        import torch
+        out = torch.zeros(max((n_tokens + 15) // 16, 1), dtype=torch.int64,
+                          device=torch.device("cuda", self.device))
+        self._check(self.lib.solid_block_keys(self.h, ctypes.c_void_p(out.data_ptr()),
+                                              self._stream(stream)))
+        return out
 
     def dump_ex(self) -> np.ndarray:
         """Evict mode: live entries with their LRU clock (ENTRY_EX_DTYPE), sorted by key."""

@@ -1790,6 +1790,44 @@ extern "C" solid_status solid_debug_counters(solid_ctx* ctx, unsigned long long*
 #endif
 }
 
+// Block table of the last batch: the key of the entry that holds each block's KV.
+template <int POLICY>
+__global__ void __launch_bounds__(256) k_block_keys(KParams kp, unsigned long long* keys_out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= kp.n) return;
+  const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
+  if (o1 < o0) return;
+  const uint32_t n = (uint32_t)min((o1 - o0) >> 4, (uint64_t)kp.max_blocks);
+  const uint64_t blk0 = o0 >> 4;
+  const int32_t f = POLICY == SOLID_POLICY_SOLIDARITY ? (int32_t)kp.dec[j].y : -1;
+  for (uint32_t b = lane; b < n; b += 32) {
+    const uint32_t id = (f >= 1 && b >= (uint32_t)f) ? kp.iso_id[blk0 + b] : kp.id_of_block[blk0 + b];
+    keys_out[blk0 + b] = kp.cold[id].key;
+  }
+}
+
+extern "C" solid_status solid_block_keys(solid_ctx* ctx, unsigned long long* keys_out,
+                                         void* stream) {
+  if (!ctx || !keys_out) return SOLID_ERR_INVALID;
+  if (ctx->dist) return fail(ctx, SOLID_ERR_STATE, "block_keys: not available on a shard");
+  if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "block_keys with a pending lookup");
+  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
+  CK(cudaSetDevice(ctx->dev));
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t n = ctx->kp.n;
+  if (!n) return SOLID_OK;
+  const unsigned grid = (unsigned)((n * 32 + 255) / 256);
+  switch (ctx->cfg.policy) {
+    case SOLID_POLICY_APC: k_block_keys<SOLID_POLICY_APC><<<grid, 256, 0, s>>>(ctx->kp, keys_out); break;
+    case SOLID_POLICY_USER_ISOLATION:
+      k_block_keys<SOLID_POLICY_USER_ISOLATION><<<grid, 256, 0, s>>>(ctx->kp, keys_out); break;
+    default: k_block_keys<SOLID_POLICY_SOLIDARITY><<<grid, 256, 0, s>>>(ctx->kp, keys_out); break;
+  }
+  CK(cudaGetLastError());
+  return SOLID_OK;
+}
+
 extern "C" solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out) {
   if (!ctx || !out) return SOLID_ERR_INVALID;
   *out = ctx->stats;

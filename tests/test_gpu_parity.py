@@ -282,6 +282,28 @@ def test_host_buffer_admission_chunked_pipeline(u16):
     assert idx.stats()["batches"] == 4
 
 
+@pytest.mark.parametrize("policy", ["apc", "user_isolation", "solidarity"])
+def test_block_keys_table(policy):
+    """solid_block_keys: per block, the key of the entry that holds its KV — the oracle's chain
+    keys with the request's own divert depth (Shared, isolated from f, or U under isolation)."""
+    import torch
+    s = concat_streams("bk", [c1_tiny(), random_small(200, users=3, alphabet_blocks=4,
+                                                       max_blocks=6, seed=2)])
+    idx = _index(policy, [s])
+    res = _admit(idx, s)
+    keys = idx.block_keys(s.n_tokens).cpu().numpy().view(np.uint64)
+    torch.cuda.synchronize()
+    o = Oracle(16, SEED, POL[policy])
+    exp = o.process(s)
+    assert np.array_equal(res, exp)
+    for j in range(s.n_requests):
+        o0, o1 = int(s.offsets[j]), int(s.offsets[j + 1])
+        f = int(exp["divert_at"][j])
+        _, K = o.chain(s.tokens[o0:o1], int(s.users[j]), f)
+        n = int(exp["n_blocks"][j])
+        assert np.array_equal(keys[o0 // 16:o0 // 16 + n], K[:n]), j
+
+
 def test_stats_are_consistent():
     s = c1_tiny()
     got, gd, idx = gpu_run(s, "solidarity")
