@@ -370,6 +370,65 @@ def measure_hash2(dev, args, d, stream_np):
             "workload": "C2 bench batch (same inputs), hash_components=2"}
 
 
+def measure_configs(dev, args):
+    """The other BASELINE configs as timed single-GPU batches (their full-size parity tests are
+    test_c3_full_size_warm_then_timed / test_c4_full_size):
+      configs[2] C3: 10 000 users, conversations to 8 k tokens, warm phase admitted untimed
+                 (index checkpointed), then the 8 timed rounds as one 80 000-request batch;
+      configs[3] C4: 1 M requests (500 k benign + victims + 500 k colluding probes), one batch.
+    Per step the index is restored to the pre-batch state outside the CUDA events."""
+    import torch
+    import paper_2603_10726_b200 as P
+    from workloads import c3_multiturn, c4_attackers
+    out = {}
+    cs = torch.cuda.current_stream(dev)
+    for name in ("c3", "c4"):
+        if name == "c3":
+            warm, s = c3_multiturn()
+            pre = [warm]
+            desc = ("c3_multiturn: 10 000 users, warm phase untimed, timed = 8 rounds as one "
+                    f"{s.n_requests}-request batch")
+        else:
+            s, pre = c4_attackers(), []
+            desc = f"c4_attackers: {s.n_requests} requests (50 % colluding probes), one batch"
+        mt = max([s.n_tokens] + [w.n_tokens for w in pre]) + 64
+        mr = max([s.n_requests] + [w.n_requests for w in pre])
+        blocks = s.n_blocks() + sum(w.n_blocks() for w in pre)
+        idx = P.Index("solidarity", capacity_blocks=max(blocks, 1 << 20), max_batch_tokens=mt,
+                      max_batch_requests=mr, seed=SEED, device=dev.index or 0)
+        for w in pre:
+            idx.admit(**P.to_device(w, dev))
+        idx.checkpoint()
+        d = P.to_device(s, dev)
+        o = torch.empty((s.n_requests, 6), dtype=torch.int32, device=dev)
+        ms, rounds = [], []
+        for k in range(args.warmup + max(args.steps // 5, 3)):
+            idx.restore()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            idx.admit_async(d["tokens"], d["offsets"], d["users"], d["enforce"], out=o)
+            e1.record(cs)
+            idx.status()
+            if k >= args.warmup:
+                ms.append(e0.elapsed_time(e1))
+                rounds.append(idx.stats()["last_rounds"])
+        med = statistics.median(ms)
+        st = idx.stats()
+        r = P.as_numpy(o)
+        out[name] = {"workload": desc, "ms_per_batch": med, "requests_per_s": s.n_requests / (med / 1e3),
+                     "blocks_per_s": s.n_blocks() / (med / 1e3), "resolver_rounds": rounds[-1],
+                     "phases_ms": {"hash": st["ms_hash"], "resolve": st["ms_resolve"],
+                                   "commit": st["ms_commit"]},
+                     "algorithmic_bytes": st["algorithmic_bytes"],
+                     "whole_step_hbm_frac": st["algorithmic_bytes"] / (med / 1e3) / 1e9 / _peaks()[0],
+                     "diverted": int(((r["bits"] & 4) > 0).sum()),
+                     "hit_rate": float(r["reused"].sum() / max(r["n_blocks"].sum(), 1))}
+        del idx, d, o
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -537,6 +596,7 @@ def main():
     ap.add_argument("--no-activator", action="store_true")
     ap.add_argument("--no-evict", action="store_true")
     ap.add_argument("--no-policy-eval", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
@@ -719,6 +779,10 @@ def main():
     if rank == 0 and world == 1 and not args.profile and not args.no_evict:
         lru = measure_evict(dev, args)
 
+    other = None
+    if rank == 0 and world == 1 and not args.profile and not args.no_configs:
+        other = measure_configs(dev, args)
+
     peval = None
     if rank == 0 and world == 1 and not args.profile and not args.no_policy_eval:
         peval = measure_policy_eval(dev, args)
@@ -750,6 +814,7 @@ def main():
             "lru_eviction": lru,
             "hash_components_2": hash2,
             "policy_eval": peval,
+            "other_configs": other,
             "e2e": e2e,
             "gpu_launches": int(sum(launches)),
             "clocks": clocks,

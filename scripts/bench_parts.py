@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import bench
 ap = argparse.ArgumentParser()
-ap.add_argument("part", choices=["evict", "policy", "hash2"])
+ap.add_argument("part", choices=["evict", "policy", "hash2", "configs"])
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--no-cpu", action="store_true")
@@ -15,6 +15,8 @@ a = ap.parse_args()
 dev = torch.device("cuda", 0)
 if a.part == "evict":
     r = bench.measure_evict(dev, a)
+elif a.part == "configs":
+    r = bench.measure_configs(dev, a)
 elif a.part == "policy":
     r = bench.measure_policy_eval(dev, a)
 else:
