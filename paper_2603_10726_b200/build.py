@@ -24,19 +24,15 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, counters: bool = False,
-          debug_lib: str = "") -> str:
+def build(force: bool = False, verbose: bool = False, counters: bool = False) -> str:
     """counters=True builds the profiling variant lib/libsolid_counters.so (-DSOLID_COUNTERS:
     per-round path counters, perturbs timing; load it with SOLID_LIB=...)."""
     lib = LIB.replace("libsolid.so", "libsolid_counters.so") if counters else LIB
-    if debug_lib:                      # -DSOLID_EVDEBUG build (device printf), never the default
-        lib = os.path.join(os.path.dirname(LIB), debug_lib)
-    if not force and not counters and not debug_lib and not needs_build():
+    if not force and not counters and not needs_build():
         return LIB
     os.makedirs(os.path.dirname(lib), exist_ok=True)
     tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *FLAGS, *(["-DSOLID_COUNTERS"] if counters else []),
-           *(["-DSOLID_EVDEBUG"] if debug_lib else []),
            "-I", os.path.join(ROOT, "include"), "-o", tmp, *SRC]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -267,10 +267,6 @@ __device__ __forceinline__ bool init_id_at(const KParams& kp, uint32_t id, uint6
       kp.win_dense[rank] = w + 1;    // ranks are unique: the window in rank order, unsorted
       c.win = w;
     }
-#ifdef SOLID_EVDEBUG
-    printf("init id %u key %llx slot %llu p %u rank %u ebound %llu w %u\n", id,
-           (unsigned long long)key, (unsigned long long)ipos, p, rank, ebound, c.win);
-#endif
   }
   kp.cold[id] = c;
   if (present && c.win == kNone) {
