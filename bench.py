@@ -701,17 +701,19 @@ def main():
     hash_bytes = 64 * nblk + 12 * N + 4 * nblk     # tokens + offsets/users + id per block
     step_ms = tot_ms / args.steps
     roof_step = alg_bytes / (step_ms / 1e3) / 1e9
-    traffic = None
+    traffic, l2hit = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "latest_ncu.json")) as f:
             prof = json.load(f)
         traffic = prof["kernels"]["k_hash_register"][-1]["traffic"]
+        l2hit = prof["kernels"]["k_hash_register"][-1].get("l2_hit_pct")
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": "k_hash_register (hash + scan + probe/register)",
                 "achieved": hash_bytes / (hash_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": hash_bytes / (hash_ms / 1e3) / 1e9 / peak, "traffic": traffic,
                 "traffic_source": "profiles/latest_ncu.json (ncu dram__bytes_read+write, same cmd)",
+                "l2_hit_pct": l2hit,
                 "algorithmic_bytes_per_launch": hash_bytes, "launch_ms": hash_ms,
                 "share_of_step": hash_ms / step_ms, "peak_source": peak_src,
                 "whole_step": {"achieved": roof_step, "frac": roof_step / peak,
