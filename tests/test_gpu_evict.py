@@ -215,3 +215,15 @@ def test_empty_and_invalid_batches_leave_state_untouched():
     assert np.array_equal(got[1], exp)
     gd, ed = idx.dump_ex(), o.dump_ex()
     assert all(np.array_equal(gd[f], ed[f]) for f in ["key", "owner", "sharer", "last_used"])
+
+
+def test_large_batch_warp_resolver():
+    """Batches larger than the GPU's resident warps (> 4736 requests) take the warp-per-request
+    evict resolver (smaller ones a CTA per request): parity on such a batch, with evictions."""
+    s = random_small(8000, users=4, alphabet_blocks=3, max_blocks=6, seed=12)
+    whole = 0
+    for cap in (1836, 2065, 2180):          # 80-95 % of the stream's 2295 distinct keys
+        st, splits, o = run_both(s.slice(2000, 8000), "solidarity", cap, 6000, max_blocks=8,
+                                 warm=s.slice(0, 2000))
+        whole += (6000 not in splits) and st["last_evicted"] > 0
+    assert whole > 0
