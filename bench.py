@@ -489,10 +489,10 @@ def run_sharded(args, world, rank, local):
     ex = TorchExchange(shard, staging=os.environ.get("SOLID_DIST_BACKEND", "nccl") != "nccl")
     coll = {"s": 0.0}
 
-    def timed_exchange(counts):
+    def timed_exchange(counts, flags=None):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = ex.exchange(counts)
+        r = ex.exchange(counts, flags=flags)
         coll["s"] += time.perf_counter() - t0
         return r
 

@@ -108,8 +108,11 @@ class ShardedIndex:
 def run_protocol(shards_local: Sequence[ShardedIndex], begin_args, exchange, allreduce_max):
     """Drive the sharded admission for the shards owned by this process.
 
-    exchange(send_counts_per_shard) -> recv_counts_per_shard (moves the records);
-    allreduce_max(list of ints) -> global max.  Returns the per-shard result tensors."""
+    exchange(send_counts_per_shard, flags=None) -> recv_counts_per_shard (moves the records);
+    with flags (one int per local shard) it returns (recv_counts_per_shard, global max flag) —
+    the round's "some decision changed" rides on the INT exchange's counts, so no separate
+    all-reduce per round.  allreduce_max(list of ints) -> global max (the commit's overflow
+    vote).  Returns the per-shard result tensors."""
     policy = shards_local[0].policy
     counts = [s.begin(*a) for s, a in zip(shards_local, begin_args)]
     recv = exchange(counts)                                       # REG
@@ -119,8 +122,7 @@ def run_protocol(shards_local: Sequence[ShardedIndex], begin_args, exchange, all
     while True:
         outs = [s.round(t, rc) for s, rc in zip(shards_local, recv)]
         counts = [o[0] for o in outs]
-        changed = allreduce_max([o[1] for o in outs])
-        recv = exchange(counts)                                   # INT
+        recv, changed = exchange(counts, flags=[o[1] for o in outs])   # INT (+ changed)
         counts = [s.owner_ingest(t, rc) for s, rc in zip(shards_local, recv)]
         if policy != "solidarity" or (t >= 2 and not changed):
             break
@@ -141,7 +143,7 @@ def loopback_admit(shards: List[ShardedIndex], local_batches, seq_bases):
     import torch
     G = len(shards)
 
-    def exchange(send_counts):
+    def exchange(send_counts, flags=None):
         recv_counts = [[int(send_counts[s][r]) for s in range(G)] for r in range(G)]
         for r in range(G):
             for s in range(G):
@@ -149,7 +151,7 @@ def loopback_admit(shards: List[ShardedIndex], local_batches, seq_bases):
                 if k:
                     shards[r].recv_region(s, k).copy_(shards[s].send_region(r, k))
         torch.cuda.synchronize()
-        return recv_counts
+        return recv_counts if flags is None else (recv_counts, max(flags))
 
     args = [(b["tokens"], b["offsets"], b["users"], b.get("enforce"), sb)
             for b, sb in zip(local_batches, seq_bases)]
@@ -165,18 +167,22 @@ class TorchExchange:
     def __init__(self, shard: ShardedIndex, group=None, staging: bool = False):
         self.shard, self.group, self.staging = shard, group, staging
 
-    def exchange(self, send_counts_list):
+    def exchange(self, send_counts_list, flags=None):
         """Counts by all_to_all_single, records by batched point-to-point (NCCL groups them;
-        gloo supports it too, which the CPU tests use)."""
+        gloo supports it too, which the CPU tests use).  flags: this rank's flag is sent to every
+        peer in bit 62 of the counts; returns (recv_counts, max flag over all ranks)."""
         import torch
         import torch.distributed as dist
         sh = self.shard
         rank = dist.get_rank(self.group)
         send_counts = np.asarray(send_counts_list[0], dtype=np.int64)
-        sc = torch.tensor(send_counts, device="cpu" if self.staging else sh.send.device)
+        wire = send_counts | (np.int64(1) << np.int64(62)) if flags and flags[0] else send_counts
+        sc = torch.tensor(wire, device="cpu" if self.staging else sh.send.device)
         rc = torch.empty_like(sc)
         dist.all_to_all_single(rc, sc, group=self.group)
-        recv_counts = rc.cpu().numpy()
+        got = rc.cpu().numpy()
+        recv_counts = got & ((np.int64(1) << np.int64(62)) - 1)
+        gflag = int((got >> np.int64(62)).max()) if flags is not None else None
         if self.staging and sh.send.is_cuda:
             torch.cuda.synchronize()
         ops, landing = [], []
@@ -203,7 +209,7 @@ class TorchExchange:
             dst.copy_(buf)
         if sh.send.is_cuda:
             torch.cuda.synchronize()
-        return [recv_counts]
+        return [recv_counts] if flags is None else ([recv_counts], gflag)
 
     def allreduce_max(self, xs):
         import torch
