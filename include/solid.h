@@ -207,6 +207,10 @@ solid_status solid_admit_host_u16(solid_ctx* ctx, const solid_batch_u16* host_ba
 
 solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out);
 
+/* Test hook: set the batch-scratch epoch (tags restart, with a scratch re-initialisation, after
+ * ~2^20 batches; tests jump close to the limit).  SOLID_ERR_STATE with a batch in flight. */
+solid_status solid_debug_set_epoch(solid_ctx* ctx, uint32_t epoch);
+
 /* Block table of the last admitted batch (paged-KV integration; call after
  * solid_insert_batch, or after solid_batch_status collected the last solid_admit_batch, and
  * before the next lookup): for request j and its block b < n_j,

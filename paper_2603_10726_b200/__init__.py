@@ -30,7 +30,7 @@ ENTRY_EX_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4"),
 # C ABI entry points declared in include/solid.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
                "solid_insert_batch", "solid_admit_host", "solid_admit_host_u16", "solid_stats", "solid_dump", "solid_dump_ex",
-               "solid_admit_batch", "solid_batch_status", "solid_block_keys",
+               "solid_admit_batch", "solid_batch_status", "solid_block_keys", "solid_debug_set_epoch",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
                "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit",
@@ -123,6 +123,8 @@ def load_library(path: str = LIB_PATH):
     lib.solid_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
     lib.solid_dump.restype = st
     lib.solid_dump.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+    lib.solid_debug_set_epoch.restype = st
+    lib.solid_debug_set_epoch.argtypes = [vp, ctypes.c_uint32]
     lib.solid_block_keys.restype = st
     lib.solid_block_keys.argtypes = [vp, vp, vp]
     lib.solid_dump_ex.restype = st
@@ -337,6 +339,10 @@ class Index:
 
     def reset(self):
         self._check(self.lib.solid_reset(self.h))
+
+    def debug_set_epoch(self, epoch: int):
+        """Test hook (solid_debug_set_epoch): jump the scratch epoch towards its restart."""
+        self._check(self.lib.solid_debug_set_epoch(self.h, epoch))
 
     def checkpoint(self):
         self._check(self.lib.solid_checkpoint(self.h))

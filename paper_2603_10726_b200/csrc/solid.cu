@@ -1892,6 +1892,15 @@ extern "C" solid_status solid_admit_host_u16(solid_ctx* ctx, const solid_batch_u
 }
 
 // Profiling build (-DSOLID_COUNTERS) only: the last collected batch's per-round path counters.
+// Test hook: move the scratch epoch (the tag space restarts after kMaxEpoch batches, ~1 M; a
+// long-running server crosses it, so the restart is tested by jumping close to it).
+extern "C" solid_status solid_debug_set_epoch(solid_ctx* ctx, uint32_t epoch) {
+  if (!ctx || epoch > kMaxEpoch) return SOLID_ERR_INVALID;
+  if (ctx->pending || ctx->outstanding) return fail(ctx, SOLID_ERR_STATE, "batch in flight");
+  ctx->epoch = epoch;
+  return SOLID_OK;
+}
+
 extern "C" solid_status solid_debug_counters(solid_ctx* ctx, unsigned long long* out) {
 #ifdef SOLID_COUNTERS
   if (!ctx || !out) return SOLID_ERR_INVALID;

@@ -304,6 +304,34 @@ def test_block_keys_table(policy):
         assert np.array_equal(keys[o0 // 16:o0 // 16 + n], K[:n]), j
 
 
+@pytest.mark.parametrize("evict", [False, True])
+def test_scratch_epoch_restart(evict):
+    """The batch-scratch tag space restarts after ~2^20 batches (a long-running server crosses
+    it): batches admitted across the restart still match the oracle, with and without LRU."""
+    import torch
+    import paper_2603_10726_b200 as P
+    s = random_small(300, users=3, alphabet_blocks=4, max_blocks=6, seed=6)
+    cap = 40 if evict else 1 << 12
+    idx = P.Index("solidarity", capacity_blocks=cap, max_batch_tokens=1 << 16,
+                  max_batch_requests=64, max_blocks=8, seed=SEED, evict=evict)
+    kmax = 0xFFFFFFFF // 4096 - 1
+    idx.debug_set_epoch(kmax - 3)
+    got = []
+    for lo in range(0, 300, 30):
+        b = s.slice(lo, lo + 30)
+        try:
+            got.append(P.as_numpy(idx.admit(**P.to_device(b))))
+        except P.SolidError as e:             # evict: a batch that must split
+            assert evict and e.status == P.SOLID_ERR_CAPACITY
+            got += [P.as_numpy(idx.admit(**P.to_device(b.slice(q, q + 1)))) for q in range(30)]
+    torch.cuda.synchronize()
+    o = Oracle(16, SEED, 2, capacity=cap if evict else 0)
+    assert np.array_equal(np.concatenate(got), o.process(s))
+    gd = idx.dump_ex() if evict else idx.dump()
+    ed = o.dump_ex() if evict else o.dump()
+    assert all(np.array_equal(gd[f], ed[f]) for f in ed.dtype.names)
+
+
 def test_stats_are_consistent():
     s = c1_tiny()
     got, gd, idx = gpu_run(s, "solidarity")
