@@ -119,6 +119,27 @@ def test_empty_and_degenerate_requests():
         assert_same(got, exp, gd, ed, f"degenerate-{policy}")
 
 
+def test_max_blocks_boundary():
+    """A request of exactly max_blocks full blocks (plus a tail) is admitted and matches the
+    oracle; one block more is SOLID_ERR_INVALID with the index untouched."""
+    import paper_2603_10726_b200 as P
+    from workloads.gen import _pack, run
+    mb = 64
+    ok = [run(1, 5, i, 16 * mb + 7) for i in range(3)] + [run(1, 5, 0, 16 * mb)]
+    s = _pack("maxb", ok, [0, 1, 2, 1])
+    idx = P.Index("solidarity", capacity_blocks=1 << 12, max_batch_tokens=1 << 16,
+                  max_batch_requests=16, max_blocks=mb, seed=SEED)
+    got = _admit(idx, s)
+    exp, ed = oracle_run(s, "solidarity")
+    assert_same(got, exp, idx.dump(), ed, "max_blocks")
+    before = idx.dump()
+    bad = _pack("over", [run(1, 6, 0, 16 * (mb + 1))], [3])
+    with pytest.raises(P.SolidError) as ei:
+        _admit(idx, bad)
+    assert ei.value.status == P.SOLID_ERR_INVALID
+    assert (idx.dump() == before).all()
+
+
 def test_empty_batch():
     import torch
     import paper_2603_10726_b200 as P
