@@ -22,7 +22,8 @@
 //  (H-def v3): both chains against their closed forms, exhaustive no-collision, decision
 //  invariance (tests/test_oracle_hash2.py).
 //  "parity unpinned": fmix64 outputs (an arbitrary finaliser; pinned only by bijectivity and by
-//  agreement with the independent CUDA implementation).
+//  agreement with the independent CUDA implementation), and likewise the H-def v3 combination
+//  key2_of (its chains S, S2 are pinned; the mixing of the two is not).
 // ============================================================================================
 #include <algorithm>
 #include <cstdint>
