@@ -191,6 +191,7 @@ class Index:
         self.device = device
         self.policy = policy
         self.seed = seed
+        self.evict = evict
 
     def close(self):
         if getattr(self, "h", None):
@@ -240,6 +241,29 @@ class Index:
         out = self.lookup(tokens, offsets, users, enforce, out, stream)
         self.insert(stream)
         return out
+
+    def admit_split(self, tokens, offsets, users, enforce=None, stream=None):
+        """Evict mode: admit, and if the batch would have to evict entries it touched itself
+        (SOLID_ERR_CAPACITY, nothing mutated) admit its two halves in order instead — the same
+        results as one request at a time (reading R1).  Returns the result tensor [N, 6]."""
+        import torch
+        try:
+            return self.admit(tokens, offsets, users, enforce, None, stream)
+        except SolidError as e:
+            n = int(users.numel())
+            if not self.evict or e.status != SOLID_ERR_CAPACITY or n < 2:
+                raise
+        h = n // 2
+        off = offsets.to(torch.int64)
+        parts = []
+        for lo, hi in ((0, h), (h, n)):
+            t0, t1 = int(off[lo]), int(off[hi])
+            parts.append(self.admit_split(tokens[t0:t1] if t1 > t0 else tokens[:4],
+                                          (off[lo:hi + 1] - t0).contiguous(),
+                                          users[lo:hi].contiguous(),
+                                          None if enforce is None else enforce[lo:hi].contiguous(),
+                                          stream).clone())
+        return torch.cat(parts)
 
     def admit_async(self, tokens, offsets, users, enforce=None, out=None, stream=None):
         """Lookup + insert without a host synchronisation (solid_admit_batch): the capacity

@@ -227,3 +227,20 @@ def test_large_batch_warp_resolver():
                                  warm=s.slice(0, 2000))
         whole += (6000 not in splits) and st["last_evicted"] > 0
     assert whole > 0
+
+
+def test_admit_split_binding():
+    """Index.admit_split bisects a batch the evict path rejects (SOLID_ERR_CAPACITY) and gives
+    the oracle's results."""
+    import torch
+    import paper_2603_10726_b200 as P
+    s = random_small(400, users=3, alphabet_blocks=5, max_blocks=6, seed=14)
+    idx = P.Index("solidarity", capacity_blocks=16, max_batch_tokens=1 << 16,
+                  max_batch_requests=512, max_blocks=8, seed=SEED, evict=True)
+    d = P.to_device(s)
+    got = P.as_numpy(idx.admit_split(d["tokens"], d["offsets"], d["users"], d["enforce"]))
+    torch.cuda.synchronize()
+    o = Oracle(16, SEED, 2, capacity=16)
+    assert np.array_equal(got, o.process(s))
+    assert all(np.array_equal(idx.dump_ex()[f], o.dump_ex()[f])
+               for f in ["key", "owner", "sharer", "last_used"])
