@@ -76,12 +76,15 @@ struct DevStatus {
   unsigned long long live_after;         // asynchronous admission: live entries after this batch
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
-  uint32_t changed[kMaxRounds + 2];
   uint32_t seg[kNSeg];                   // id counts per segment (gathered by k_stats)
 #ifdef SOLID_COUNTERS
   unsigned long long cnt[16][8];         // profiling build only: per-round path counters
 #endif
+  // last: round t's "some decision changed" holds the batch epoch (never reset; a stale value
+  // can only cost one certifying round), so a batch clears and copies only the head above
+  uint32_t changed[kMaxRounds + 2];
 };
+constexpr size_t kStHead = offsetof(DevStatus, changed);
 
 struct KParams {
   int policy;
@@ -958,7 +961,7 @@ __global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) 
     // one store per CTA (100k same-address stores would serialise on one L2 slice)
     if (lane == 0 && any) s_changed = 1;
     __syncthreads();
-    if (threadIdx.x == 0 && s_changed) kp.st->changed[t] = 1;
+    if (threadIdx.x == 0 && s_changed) kp.st->changed[t] = kp.epoch;
     if (POLICY != SOLID_POLICY_SOLIDARITY) {         // exact in one pass
       if (grid.thread_rank() == 0) kp.st->conv = 1;
       return;
@@ -970,7 +973,7 @@ __global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) 
     // one L2 read per CTA, broadcast through shared memory
     __shared__ uint32_t s_ch, s_er;
     if (threadIdx.x == 0) {
-      s_ch = *(volatile uint32_t*)&kp.st->changed[t];
+      s_ch = *(volatile uint32_t*)&kp.st->changed[t] == kp.epoch;
       s_er = *(volatile uint32_t*)&kp.st->err;
     }
     __syncthreads();
@@ -1324,6 +1327,7 @@ static solid_status init_scratch(solid_ctx* ctx, cudaStream_t s) {
                                   ctx->idcap * (sizeof(Hot) / 8), ~0ull);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
+  if (ctx->st) CK(cudaMemsetAsync(ctx->st, 0, sizeof(DevStatus), s));   // changed[] is epoch-tagged
   if (ctx->ev_state) {                       // id publication words carry the epoch
     solid_status rc = evict_scratch_reset(ctx, s);
     if (rc != SOLID_OK) return rc;
@@ -1573,7 +1577,7 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   kp.seg_cnt = ctx->seg_cnt;
   kp.seg_cap = ctx->seg_cap;
   kp.st = ctx->st;
-  CK(cudaMemsetAsync(ctx->st, 0, sizeof(DevStatus), s));
+  CK(cudaMemsetAsync(ctx->st, 0, kStHead, s));
   CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
   if (ctx->ev_state) return evict_lookup(ctx, s);
   CK(cudaEventRecord(ctx->ev[0], s));
@@ -1633,7 +1637,7 @@ static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mo
     }
   }
   CK(cudaEventRecord(ctx->ev[3], s));
-  CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ctx->st_host, ctx->st, kStHead, cudaMemcpyDeviceToHost, s));
   CK(cudaEventRecord(ctx->ev[6], s));
   Flight& f = ctx->fl[ctx->cur];
   f.n = n;
