@@ -1082,12 +1082,36 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
   }
 }
 
+// Exact rollback of a committed batch by one CTA (the asynchronous path's device-decided
+// capacity overflow, R9): every slot the batch claimed was EMPTY before — empty it again — and
+// every sharer it wrote was NONE.  Rare (an error path), so a single CTA is enough.
+__device__ void rollback_all(const KParams& kp) {
+  const uint32_t tf = kp.st->conv == 0 ? 0 : (POLICY_IS_SOLIDARITY(kp) ? kp.st->conv : 0);
+  const int W = (int)(tf & 1);
+  const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
+  for (uint32_t seg = 0; seg < (uint32_t)kNSeg; ++seg) {
+    const uint32_t cnt = min(kp.seg_cnt[seg].v, kp.seg_cap);
+    for (uint32_t x = threadIdx.x; x < cnt; x += blockDim.x) {
+      const uint32_t id = seg * kp.seg_cap + x + 1;
+      const ulonglong2 pw = ldw128(&kp.hot[id].v[2 * W]);
+      const uint32_t itag = (uint32_t)(pw.x >> 32);
+      if (itag == tag) {
+        kp.tab[kp.cold[id].psl] = make_ulonglong2(0ull, 0ull);
+      } else if (itag == tagS && (uint32_t)(pw.y >> 32) == tag) {
+        uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
+        atomicCAS(sharer_word, kp.users[(uint32_t)pw.y - 1u], kNone);
+      }
+    }
+  }
+}
+
 // Per-batch sums over the results (block-weighted hit rate).
 // With `live` set (asynchronous admission) the last CTA also takes the capacity decision (R9):
 // the live count stays resident on the device and an overflow is flagged for the rollback.
 __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t n,
                                                DevStatus* st, unsigned long long* live,
-                                               unsigned long long cap, const SegCounter* seg) {
+                                               unsigned long long cap, const SegCounter* seg,
+                                               KParams kp) {
   if (blockIdx.x == 0 && threadIdx.x < kNSeg) st->seg[threadIdx.x] = seg[threadIdx.x].v;
   unsigned long long a[6] = {0, 0, 0, 0, 0, 0};
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
@@ -1111,18 +1135,26 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
   __syncthreads();
   if (threadIdx.x < 6 && s_a[threadIdx.x]) atomicAdd(&st->sums[threadIdx.x], s_a[threadIdx.x]);
   if (!live) return;
-  __shared__ bool s_last;
+  __shared__ bool s_last, s_ovf;
   if (threadIdx.x == 0) s_last = atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {   // new_entries is final: k_commit completed before us
+  if (!s_last) return;
+  if (threadIdx.x == 0) {             // new_entries is final: k_commit completed before us
     __threadfence();
+    s_ovf = false;
     if (!st->err) {
       const unsigned long long l = *live, add = st->new_entries;
-      if (l + add > cap) st->overflow = 1;
-      else *live = l + add;
+      if (l + add > cap) {
+        st->overflow = 1;
+        s_ovf = true;
+      } else {
+        *live = l + add;
+      }
     }
     st->live_after = *live;
   }
+  __syncthreads();
+  if (s_ovf) rollback_all(kp);        // the batch leaves the index exactly as before it
 }
 
 // Compact the live index slots (dump): warp-aggregated append.
@@ -1625,16 +1657,13 @@ static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mo
     launch_commit(ctx, 1, s);      // optimistic commit + count; exact rollback on overflow
     CK(cudaGetLastError());
     // asynchronous: k_stats' last CTA also takes the capacity decision on the device
+    // asynchronous: k_stats' last CTA also takes the capacity decision and, on overflow, rolls
+    // the batch back itself (no extra launch per batch)
     k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
         ctx->kp.out, n, ctx->st, async_mode ? ctx->live_dev : nullptr, ctx->cfg.capacity_blocks,
-        ctx->seg_cnt);
+        ctx->seg_cnt, ctx->kp);
     CK(cudaGetLastError());
     ctx->launches += 2;
-    if (async_mode) {
-      launch_commit(ctx, 3, s);    // rolls back only if the device saw an overflow
-      CK(cudaGetLastError());
-      ctx->launches += 1;
-    }
   }
   CK(cudaEventRecord(ctx->ev[3], s));
   CK(cudaMemcpyAsync(ctx->st_host, ctx->st, kStHead, cudaMemcpyDeviceToHost, s));
