@@ -111,3 +111,22 @@ def test_c2_full_size_sharded_two_shards():
     exp, ed = oracle_run([s], "solidarity")
     got, gd, rounds = sharded_run([s], 2, "solidarity")
     assert_same(got, exp, gd, ed, "c2full G=2")
+
+
+def test_fuzz_sharded():
+    """Seeded random cases for the sharded protocol (loopback): G in 2..5 shards, random
+    policy, streams cut into several global batches — results and the union of the shards bit
+    exact against the oracle."""
+    rng = np.random.default_rng(77)
+    for case in range(24):
+        G = int(rng.integers(2, 6))
+        policy = list(POL)[int(rng.integers(3))]
+        s = random_small(int(rng.integers(20, 200)), users=int(rng.integers(1, 6)),
+                         alphabet_blocks=int(rng.integers(2, 6)), max_blocks=int(rng.integers(1, 9)),
+                         seed=1000 + case, enforce_prob=float(rng.choice([1.0, 0.6])))
+        k = int(rng.integers(1, 4))
+        cuts = sorted(set([0, s.n_requests] + list(rng.integers(0, s.n_requests, k - 1))))
+        streams = [s.slice(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+        got, gd, _ = sharded_run(streams, G, policy)
+        exp, ed = oracle_run(streams, policy)
+        assert_same(got, exp, gd, ed, f"fuzz{case}-G{G}-{policy}")
