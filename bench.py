@@ -701,12 +701,13 @@ def main():
     hash_bytes = 64 * nblk + 12 * N + 4 * nblk     # tokens + offsets/users + id per block
     step_ms = tot_ms / args.steps
     roof_step = alg_bytes / (step_ms / 1e3) / 1e9
-    traffic, l2hit = None, None
+    traffic, l2hit, res_inst = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "latest_ncu.json")) as f:
             prof = json.load(f)
         traffic = prof["kernels"]["k_hash_register"][-1]["traffic"]
         l2hit = prof["kernels"]["k_hash_register"][-1].get("l2_hit_pct")
+        res_inst = prof["kernels"]["k_resolve"][-1].get("warp_instructions")
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": "k_hash_register (hash + scan + probe/register)",
@@ -719,6 +720,20 @@ def main():
                 "whole_step": {"achieved": roof_step, "frac": roof_step / peak,
                                "algorithmic_bytes": alg_bytes,
                                "resolver_share": statistics.median(phase["resolve"]) / step_ms}}
+
+    # the resolver (the largest share of the step, no algorithmic bytes) is bound by instruction
+    # issue: its warp instructions per launch (ncu, same batch) over its measured time, against
+    # 148 SMs x 4 schedulers x one warp instruction per clock at the sampled SM clock
+    resolver_roofline = None
+    if res_inst:
+        res_ms = statistics.median(phase["resolve"])
+        clk = (clocks or {}).get("sm_mhz") or 1965.0
+        peak_issue = 148 * 4 * clk * 1e6
+        resolver_roofline = {"bound": "issue", "kernel": "k_resolve (all rounds, one launch)",
+                             "achieved": res_inst / (res_ms / 1e3) / 1e12, "peak": peak_issue / 1e12,
+                             "unit": "T warp instr/s", "frac": res_inst / (res_ms / 1e3) / peak_issue,
+                             "warp_instructions_per_launch": res_inst,
+                             "source": "profiles/latest_ncu.json (smsp__inst_executed.sum)"}
 
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
     e2e = None
@@ -811,6 +826,7 @@ def main():
                        "submission": "solid_admit_batch pipelined: step k+1 enqueued before "
                                      "step k's status is collected"},
             "roofline": roofline,
+            "resolver_roofline": resolver_roofline,
             "cpu_baseline": cpu,
             "activator": activator,
             "lru_eviction": lru,

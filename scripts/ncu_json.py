@@ -33,6 +33,8 @@ for i, n, m in second:
     for k, name in [("dram__bytes_read.sum", "dram_read"), ("dram__bytes_write.sum", "dram_write")]:
         if k in m:
             d[name] = int(float(m[k][0].replace(",", "")) * scale.get(m[k][1], 1))
+    if "smsp__inst_executed.sum" in m:
+        d["warp_instructions"] = int(float(m["smsp__inst_executed.sum"][0].replace(",", "")))
     if "lts__t_sector_hit_rate.pct" in m:
         d["l2_hit_pct"] = round(float(m["lts__t_sector_hit_rate.pct"][0].replace(",", "")), 1)
     if "dram_read" in d and "dram_write" in d:
