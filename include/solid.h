@@ -73,7 +73,7 @@ typedef struct {
                                   B2) mixed into every key — the chain collision bound drops from
                                   ~L/2^61 to ~L^2/2^122 per pair (L = tokens), below the 64-bit
                                   key's 2^-64.  Decisions are unchanged (absent collisions); keys
-                                  differ.  world == 1 only.                                       */
+                                  differ.  Also with the sharded index (world > 1).              */
 } solid_config;
 
 typedef struct solid_ctx solid_ctx;

@@ -1386,8 +1386,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   if (world > 64 || cfg->rank >= world) return SOLID_ERR_INVALID;
   if (cfg->evict > 1 || (cfg->evict && (world != 1 || cfg->capacity_blocks < cfg->max_blocks)))
     return SOLID_ERR_INVALID;
-  if (cfg->hash_components > 2 || (cfg->hash_components == 2 && world != 1))
-    return SOLID_ERR_INVALID;
+  if (cfg->hash_components > 2) return SOLID_ERR_INVALID;
   ctx = new solid_ctx();
   ctx->cfg = *cfg;
   ctx->cfg.world = world;

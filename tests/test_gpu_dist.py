@@ -13,13 +13,14 @@ SEED = 0x5011D000
 POL = {"apc": 0, "user_isolation": 1, "solidarity": 2}
 
 
-def _shards(G, policy, streams):
+def _shards(G, policy, streams, nc=1):
     from paper_2603_10726_b200.dist import ShardedIndex
     tok = max(max(s.n_tokens for s in streams), 64)
     req = max(max(s.n_requests for s in streams), 1)
     blocks = sum(s.n_blocks() for s in streams)
     return [ShardedIndex(G, r, policy, capacity_blocks=max(4 * blocks, 4096),
-                         max_batch_tokens=tok + 64, max_batch_requests=req, seed=SEED)
+                         max_batch_tokens=tok + 64, max_batch_requests=req, seed=SEED,
+                         hash_components=nc)
             for r in range(G)]
 
 
@@ -29,11 +30,11 @@ def _split(s, G):
     return [s.slice(cuts[r], cuts[r + 1]) for r in range(G)], cuts[:-1]
 
 
-def sharded_run(streams, G, policy):
+def sharded_run(streams, G, policy, nc=1):
     import torch
     import paper_2603_10726_b200 as P
     from paper_2603_10726_b200.dist import loopback_admit
-    shards = _shards(G, policy, streams)
+    shards = _shards(G, policy, streams, nc)
     out, rounds = [], []
     seq = 0
     for s in streams:
@@ -130,3 +131,14 @@ def test_fuzz_sharded():
         got, gd, _ = sharded_run(streams, G, policy)
         exp, ed = oracle_run(streams, policy)
         assert_same(got, exp, gd, ed, f"fuzz{case}-G{G}-{policy}")
+
+
+@pytest.mark.parametrize("policy", list(POL))
+def test_two_component_keys_sharded(policy):
+    """H-def v3 keys with the sharded index (G = 3): results and the shard union (keys
+    included) equal the oracle with components=2."""
+    s = random_small(300, users=4, alphabet_blocks=3, max_blocks=10, seed=31, enforce_prob=0.8)
+    got, gd, _ = sharded_run([s.slice(0, 150), s.slice(150, 300)], 3, policy, nc=2)
+    o = Oracle(16, SEED, POL[policy], components=2)
+    exp = np.concatenate([o.process(s.slice(0, 150)), o.process(s.slice(150, 300))])
+    assert_same(got, exp, gd, o.dump(), f"v3-sharded-{policy}")
