@@ -74,6 +74,12 @@ def _load():
         lib.oracle_chain2.argtypes = [vp, vp, u32, u32, i32, vp, vp, vp]
         lib.oracle_dump_ex.restype = u64
         lib.oracle_dump_ex.argtypes = [vp, vp, u64]
+        lib.oracle_set_pool.restype = ctypes.c_int
+        lib.oracle_set_pool.argtypes = [vp, u64]
+        lib.oracle_block_table.restype = u64
+        lib.oracle_block_table.argtypes = [vp, vp, u64]
+        lib.oracle_dump_phys.restype = u64
+        lib.oracle_dump_phys.argtypes = [vp, vp, vp, u64]
         _lib = lib
     return _lib
 
@@ -86,7 +92,7 @@ class Oracle:
     """Sequential reference: Oracle(block_size, seed, policy).process(stream) -> results."""
 
     def __init__(self, block_size: int = 16, seed: int = 0, policy: int = POLICY_SOLIDARITY,
-                 capacity: int = 0, components: int = 1):
+                 capacity: int = 0, components: int = 1, pool: int = 0):
         self.lib = _load()
         self.block_size, self.seed, self.policy = block_size, seed, policy
         self.h = self.lib.oracle_create(block_size, seed & 0xFFFFFFFFFFFFFFFF, policy)
@@ -98,6 +104,9 @@ class Oracle:
             raise ValueError("components must be 1 or 2")
         if capacity:
             self.lib.oracle_set_capacity(self.h, capacity)   # LRU eviction (R22-R25)
+        self.pool = pool
+        if pool and self.lib.oracle_set_pool(self.h, pool):  # physical blocks (R26-R28)
+            raise ValueError("bad pool size")
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -117,6 +126,8 @@ class Oracle:
             tokens = np.zeros(1, dtype=np.uint32)
         err = self.lib.oracle_process(self.h, n, _ptr(tokens), _ptr(offsets), _ptr(users),
                                       _ptr(en), _ptr(out))
+        if err == 4:
+            raise ValueError("oracle_process: physical block pool exhausted")
         if err:
             raise ValueError(f"oracle_process: invalid batch (code {err})")
         return out
@@ -148,6 +159,21 @@ class Oracle:
         out = np.zeros(max(n, 1), dtype=ENTRY_EX_DTYPE)
         self.lib.oracle_dump_ex(self.h, _ptr(out), n)
         return out[:n]
+
+    def block_table(self) -> np.ndarray:
+        """Block table of the last process call (R27): index offsets[j] // 16 + b."""
+        n = int(self.lib.oracle_block_table(self.h, None, 0))
+        out = np.zeros(max(n, 1), dtype=np.uint32)
+        self.lib.oracle_block_table(self.h, _ptr(out), n)
+        return out[:n]
+
+    def dump_phys(self):
+        """(keys, physical blocks) of the live entries, sorted by key."""
+        n = self.size()
+        k = np.zeros(max(n, 1), dtype=np.uint64)
+        p = np.zeros(max(n, 1), dtype=np.uint32)
+        self.lib.oracle_dump_phys(self.h, _ptr(k), _ptr(p), n)
+        return k[:n], p[:n]
 
     def evictions(self) -> int:
         return int(self.lib.oracle_evictions(self.h))

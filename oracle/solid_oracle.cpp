@@ -20,7 +20,9 @@
 //  SPEC evict_lru S:117-125): the SPEC examples, Mattson's stack-distance theorem, the cyclic
 //  thrash closed form, a brute-force trie LRU (tests/test_oracle_eviction.py).  Two-component keys
 //  (H-def v3): both chains against their closed forms, exhaustive no-collision, decision
-//  invariance (tests/test_oracle_hash2.py).
+//  invariance (tests/test_oracle_hash2.py).  Physical block pool and block tables (R26-R28): the
+//  first-insertion and cyclic-thrash closed forms, a brute-force min-stamp allocator over the
+//  trie, lifetime invariants (tests/test_oracle_pool.py).
 //  "parity unpinned": fmix64 outputs (an arbitrary finaliser; pinned only by bijectivity and by
 //  agreement with the independent CUDA implementation), and likewise the H-def v3 combination
 //  key2_of (its chains S, S2 are pinned; the mixing of the two is not).
@@ -28,6 +30,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <deque>
 #include <set>
 #include <unordered_map>
 #include <utility>
@@ -74,6 +77,7 @@ struct Entry {
   uint32_t sharer;    // user that flagged the entry; AttackFlag <=> sharer != NONE (R5)
   uint64_t last_used; // LRU clock (R22): global sequence number of the last request
                       // that was served this entry or inserted it
+  uint32_t phys;      // physical KV block holding the entry's content (R26); NONE = pool off
 };
 
 struct Ctx {
@@ -95,6 +99,14 @@ struct Ctx {
   uint64_t capacity;
   std::set<std::pair<uint64_t, uint64_t>> lru;
   uint64_t evictions;
+  // Physical block pool (the vLLM block manager beneath the prefix index, P:733;
+  // DESIGN.md R26-R28).  pool 0 = off.  A FIFO of free physical block ids, initially 0..pool-1:
+  // an evicted entry's block goes to the back; a request's new entries take blocks from the
+  // front, in block order, after the request's own evictions returned theirs (R26).
+  uint64_t pool;
+  std::deque<uint32_t> freeq;
+  std::vector<uint64_t> fresh;        // keys the current request inserted, in block order
+  std::vector<uint32_t> btab;         // block table of the last oracle_process call (R27)
 };
 
 uint64_t sigma_of(const Ctx& c, uint32_t user) {
@@ -144,8 +156,9 @@ uint32_t owner_of(const Ctx& c, uint64_t key) { return c.table.at(key).owner; }
 // it unchanged — owner, flag and last_used (R8, R23).
 void insert_if_absent(Ctx& c, uint64_t key, uint32_t user, uint64_t seq) {
   if (present(c, key)) return;
-  c.table.emplace(key, Entry{user, (uint32_t)NONE, seq});
+  c.table.emplace(key, Entry{user, (uint32_t)NONE, seq, (uint32_t)NONE});
   if (c.capacity) c.lru.insert(std::make_pair(seq, key));
+  if (c.pool) c.fresh.push_back(key);
 }
 
 // An entry whose cached content is served to the request refreshes its last_used (R23).
@@ -166,6 +179,7 @@ void evict_to_capacity(Ctx& c) {
   if (!c.capacity) return;
   while (c.table.size() > c.capacity) {
     auto victim = c.lru.begin();
+    if (c.pool) c.freeq.push_back(c.table.at(victim->second).phys);   // its block is free again
     c.table.erase(victim->second);
     c.lru.erase(victim);
     ++c.evictions;
@@ -212,6 +226,7 @@ void* oracle_create(uint32_t block_size, uint64_t seed, int policy) {
   c->next_seq = 0;
   c->capacity = 0;
   c->evictions = 0;
+  c->pool = 0;
   return c;
 }
 
@@ -224,6 +239,39 @@ int oracle_set_capacity(void* h, uint64_t capacity) {
 }
 
 uint64_t oracle_evictions(void* h) { return ((Ctx*)h)->evictions; }
+
+// Physical block pool of `pool` blocks (R26-R28; 0 = off).  Must be set on an empty table.
+int oracle_set_pool(void* h, uint64_t pool) {
+  Ctx* c = (Ctx*)h;
+  if (!c->table.empty() || pool >= NONE) return 1;
+  c->pool = pool;
+  c->freeq.clear();
+  for (uint64_t i = 0; i < pool; ++i) c->freeq.push_back((uint32_t)i);
+  return 0;
+}
+
+// Block table of the last oracle_process call: entry offsets[j]/bs + b-1 = the physical block of
+// request j's block b (R27); positions no request's full block covers hold NONE.  Returns the
+// number of positions (writes at most cap).
+uint64_t oracle_block_table(void* h, uint32_t* out, uint64_t cap) {
+  Ctx* c = (Ctx*)h;
+  const uint64_t n = std::min<uint64_t>(cap, c->btab.size());
+  if (n) std::memcpy(out, c->btab.data(), n * sizeof(uint32_t));
+  return c->btab.size();
+}
+
+// Live entries' physical blocks, sorted by key.
+uint64_t oracle_dump_phys(void* h, uint64_t* keys, uint32_t* phys, uint64_t cap) {
+  Ctx& c = *(Ctx*)h;
+  std::vector<std::pair<uint64_t, uint32_t>> v;
+  for (auto& kv : c.table) v.push_back(std::make_pair(kv.first, kv.second.phys));
+  std::sort(v.begin(), v.end());
+  for (uint64_t i = 0; i < std::min<uint64_t>(cap, v.size()); ++i) {
+    keys[i] = v[i].first;
+    phys[i] = v[i].second;
+  }
+  return v.size();
+}
 
 // H-def components (1 or 2).  Must be set on an empty table.
 int oracle_set_components(void* h, int components) {
@@ -305,6 +353,7 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
   if (err) return err;
   std::vector<uint64_t> hsh, hsh2, S, S2, Kk, I;
   const bool two = c.components == 2;
+  if (c.pool) c.btab.assign(n_req ? (offsets[n_req] + c.bs - 1) / c.bs : 0, (uint32_t)NONE);
   for (uint64_t j = 0; j < n_req; ++j, ++c.next_seq) {
     const uint32_t u = users[j];
     const bool e = enforce ? enforce[j] != 0 : true;
@@ -319,6 +368,7 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
 
     uint32_t k = 0, r = 0, flagd = 0;
     int32_t f = -1;
+    c.fresh.clear();
 
     if (c.policy == 1) {
       // USER_ISOLATION baseline: a per-user namespace from the root.
@@ -419,6 +469,23 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
       }
     }
     evict_to_capacity(c);
+    if (c.pool) {
+      // R26: the request's new entries take free blocks in block order (after its evictions)
+      for (uint64_t key : c.fresh) {
+        if (c.freeq.empty()) return 4;                       // pool exhausted (no eviction)
+        c.table.at(key).phys = c.freeq.front();
+        c.freeq.pop_front();
+      }
+      // R27: block table = the physical block of the entry holding each block's key as the
+      // request used it (Shared K[b] before the divert point, isolated I[b] from it, per-user
+      // I[b] under USER_ISOLATION), NONE if that entry is not live after the request
+      const uint64_t bt0 = offsets[j] / c.bs;
+      for (uint32_t b = 1; b <= n; ++b) {
+        const uint64_t key = (c.policy == 1 || (f >= 0 && (int64_t)b > (int64_t)f)) ? I[b] : Kk[b];
+        auto it = c.table.find(key);
+        c.btab[bt0 + b - 1] = it == c.table.end() ? (uint32_t)NONE : it->second.phys;
+      }
+    }
     oracle_result& o = out[j];
     o.n_blocks = n;
     o.shared_hits = (c.policy == 1) ? 0 : k;
@@ -475,6 +542,8 @@ void oracle_copy_table(void* dst, void* src) {
   d->evictions = s->evictions;
   d->next_seq = s->next_seq;
   d->components = s->components;
+  d->pool = s->pool;
+  d->freeq = s->freeq;
 }
 
 void oracle_reserve(void* h, uint64_t n) { ((Ctx*)h)->table.reserve(n); }

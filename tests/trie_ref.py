@@ -20,7 +20,8 @@ class TrieRef:
     smallest (last_used, key) is removed by a linear scan.  `keyfn(name)` gives the entry's hash
     value, needed only for the tie-break ("ties broken by smaller hash value")."""
 
-    def __init__(self, block_size: int = 16, policy: int = 2, capacity: int = 0, keyfn=None):
+    def __init__(self, block_size: int = 16, policy: int = 2, capacity: int = 0, keyfn=None,
+                 pool: int = 0):
         self.bs = block_size
         self.policy = policy
         self.table = {}     # name -> [owner, sharer]
@@ -29,6 +30,15 @@ class TrieRef:
         self.last_used = {}  # name -> clock
         self.clock = 0
         self.evictions = 0
+        # physical blocks (R26-R28), brute force: every block carries the event stamp at which it
+        # was last freed (never-used block i: stamp i - pool, before any event); a request's new
+        # entries each take the free block with the smallest stamp, in block order, after the
+        # request's evictions freed theirs
+        self.pool = pool
+        self.freed_at = {i: i - pool for i in range(pool)}   # free block -> stamp
+        self.phys = {}                                       # name -> block
+        self.events = 0
+        self.fresh = []
 
     def _served(self, names):
         for nm in names:
@@ -38,6 +48,7 @@ class TrieRef:
         if name not in t:
             t[name] = [u, NONE]
             self.last_used[name] = self.clock
+            self.fresh.append(name)
 
     def _evict(self):
         while self.capacity and len(self.table) > self.capacity:
@@ -45,6 +56,9 @@ class TrieRef:
             del self.table[victim]
             del self.last_used[victim]
             self.evictions += 1
+            if self.pool:
+                self.freed_at[self.phys.pop(victim)] = self.events
+                self.events += 1
 
     def _blocks(self, toks):
         n = len(toks) // self.bs
@@ -56,6 +70,7 @@ class TrieRef:
         t = self.table
         k = r = flagd = 0
         f = -1
+        self.fresh = []
         if self.policy == 1:
             names = [("I", (), u, tuple(blk[:b])) for b in range(1, n + 1)]
             while r < n and names[r] in t:
@@ -64,6 +79,7 @@ class TrieRef:
             for b in range(r, n):
                 self._insert(t, names[b], u)
             f = 0
+            used = names
         else:
             shared = [("S", tuple(blk[:b])) for b in range(1, n + 1)]
             while k < n and shared[k] in t:
@@ -73,6 +89,7 @@ class TrieRef:
                 self._served(shared[:k])
                 for b in range(k, n):
                     self._insert(t, shared[b], u)
+                used = shared
             else:
                 if e:
                     for b in range(1, k + 1):
@@ -91,6 +108,7 @@ class TrieRef:
                     self._served(shared[:k])
                     for b in range(k, n):
                         self._insert(t, shared[b], u)
+                    used = shared
                 else:
                     root = tuple(blk[:f])
                     iso = [("I", root, u, tuple(blk[f:b])) for b in range(f + 1, n + 1)]
@@ -101,7 +119,16 @@ class TrieRef:
                     self._served(shared[:f] + iso[:m])
                     for name in iso[m:]:
                         self._insert(t, name, u)
+                    used = shared[:f] + iso
         self._evict()
+        if self.pool:
+            for name in self.fresh:
+                if not self.freed_at:
+                    raise RuntimeError("pool exhausted")
+                blk_id = min(self.freed_at, key=lambda i: self.freed_at[i])
+                del self.freed_at[blk_id]
+                self.phys[name] = blk_id
+            self.table_row = [self.phys.get(nm, NONE) if nm in t else NONE for nm in used]
         self.clock += 1
         bits = ((1 if r > 0 else 0) | (2 if (n > 0 and r == n) else 0) | (4 if f >= 0 else 0)
                 | (8 if (f >= 0 and f < k) else 0) | (16 if flagd > 0 else 0))
