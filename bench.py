@@ -16,6 +16,7 @@ ranks.  `--impl reference` times the sequential CPU oracle on the same workload 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -368,6 +369,43 @@ def measure_hash2(dev, args, d, stream_np):
     return {"ms_per_step": med, "requests_per_s": N / (med / 1e3),
             "hash_kernel_ms": statistics.median(hk),
             "workload": "C2 bench batch (same inputs), hash_components=2"}
+
+
+def measure_block_table(dev, args, d, stream_np):
+    """the C2 step with physical block ids and the block table
+    (block_table=True) against the same synchronous step without — the price of
+    the allocator (pre-pass, count, scan, assign, table, copy-out)."""
+    import torch
+    import paper_2603_10726_b200 as P
+    N, nblk = stream_np.n_requests, stream_np.n_blocks()
+    cs = torch.cuda.current_stream(dev)
+    res = {}
+    for bt in (False, True):
+        idx = P.Index("solidarity", capacity_blocks=max(nblk // 6, 1 << 20),
+                      max_batch_tokens=stream_np.n_tokens + 64, max_batch_requests=N, seed=SEED,
+                      device=dev.index or 0, block_table=bt)
+        out = torch.empty((N, 6), dtype=torch.int32, device=dev)
+        table = torch.empty(((stream_np.n_tokens + 15) // 16,), dtype=torch.int32, device=dev)
+        ms = []
+        for k in range(args.warmup + max(args.steps // 5, 3)):
+            idx.reset()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            idx.admit(d["tokens"], d["offsets"], d["users"], d["enforce"], out=out)
+            if bt:
+                idx._check(idx.lib.solid_block_table(idx.h, ctypes.c_void_p(table.data_ptr()),
+                                                      idx._stream(None)))
+            e1.record(cs)
+            torch.cuda.synchronize(dev)
+            if k >= args.warmup:
+                ms.append(e0.elapsed_time(e1))
+        res["with_block_table" if bt else "without"] = statistics.median(ms)
+        idx.close()
+    res["overhead_ms"] = res["with_block_table"] - res["without"]
+    res["workload"] = ("C2 bench batch, synchronous admit (lookup + insert) "
+                       "± physical block ids + block table copy-out")
+    res["table_entries"] = nblk
+    return res
 
 
 def measure_configs(dev, args):
@@ -792,6 +830,10 @@ def main():
     if rank == 0 and world == 1 and not args.profile:
         hash2 = measure_hash2(dev, args, d, stream_np)
 
+    btab = None
+    if rank == 0 and world == 1 and not args.profile:
+        btab = measure_block_table(dev, args, d, stream_np)
+
     lru = None
     if rank == 0 and world == 1 and not args.profile and not args.no_evict:
         lru = measure_evict(dev, args)
@@ -831,6 +873,7 @@ def main():
             "activator": activator,
             "lru_eviction": lru,
             "hash_components_2": hash2,
+            "block_table": btab,
             "policy_eval": peval,
             "other_configs": other,
             "e2e": e2e,

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SOLID_ABI_VERSION 4u
+#define SOLID_ABI_VERSION 5u
 #define SOLID_USER_NONE 0xFFFFFFFFu   /* "no user": sharer of an unflagged entry */
 
 typedef enum {
@@ -74,6 +74,13 @@ typedef struct {
                                   ~L/2^61 to ~L^2/2^122 per pair (L = tokens), below the 64-bit
                                   key's 2^-64.  Decisions are unchanged (absent collisions); keys
                                   differ.  Also with the sharded index (world > 1).              */
+  uint32_t block_table;        /* 1: physical KV blocks and per-request block tables (SURVEY f4,
+                                  P:733 "vLLM" block manager, R26-R28).  A pool of
+                                  capacity_blocks physical block ids; a FIFO of free ids (initially
+                                  0..capacity_blocks-1); per request, its evictions return their
+                                  blocks first, then its new entries take blocks in block order.
+                                  See solid_block_table / solid_dump_phys.  Single GPU only;
+                                  admission synchronous (solid_admit_batch is refused).          */
 } solid_config;
 
 typedef struct solid_ctx solid_ctx;
@@ -221,6 +228,19 @@ solid_status solid_debug_set_epoch(solid_ctx* ctx, uint32_t epoch);
  * memory, ceil(total tokens / 16) entries; positions no request's full block covers are not
  * written.  Enqueued on `stream`.  Single-GPU contexts only. */
 solid_status solid_block_keys(solid_ctx* ctx, unsigned long long* keys_out, void* stream);
+
+/* Block table of the last committed batch (block_table = 1, R27): DEVICE array
+ * indexed like solid_block_keys (offsets[j]/16 + b); entry = the physical block id of the entry
+ * holding request j's block b as the request used it (Shared before the divert point, isolated
+ * from it), SOLID_USER_NONE if that entry did not survive the request (evict mode: an entry the
+ * request referenced without being served it and then evicted).  Positions no request's full
+ * block covers are not written.  The batch's offsets must still be valid.  Enqueued on stream. */
+solid_status solid_block_table(solid_ctx* ctx, uint32_t* table_out, void* stream);
+
+/* Live entries' physical blocks sorted by key (HOST arrays, capacity cap); *n_out = live
+ * entries.  block_table = 1 contexts only. */
+solid_status solid_dump_phys(solid_ctx* ctx, uint64_t* keys_out, uint32_t* phys_out, uint64_t cap,
+                             uint64_t* n_out);
 
 /* Copy live entries to host_out (HOST memory, capacity `cap` entries) sorted by key; *n_out =
  * number of live entries (may exceed cap; then only cap are written). */

@@ -31,6 +31,7 @@ ENTRY_EX_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4"),
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
                "solid_insert_batch", "solid_admit_host", "solid_admit_host_u16", "solid_stats", "solid_dump", "solid_dump_ex",
                "solid_admit_batch", "solid_batch_status", "solid_block_keys", "solid_debug_set_epoch",
+               "solid_block_table", "solid_dump_phys",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
                "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit",
@@ -52,7 +53,8 @@ class _Config(ctypes.Structure):
                 ("max_batch_requests", ctypes.c_uint64), ("hash_seed", ctypes.c_uint64),
                 ("policy", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32),
-                ("evict", ctypes.c_uint32), ("hash_components", ctypes.c_uint32)]
+                ("evict", ctypes.c_uint32), ("hash_components", ctypes.c_uint32),
+                ("block_table", ctypes.c_uint32)]
 
 
 class _Batch(ctypes.Structure):
@@ -128,6 +130,10 @@ def load_library(path: str = LIB_PATH):
     lib.solid_block_keys.restype = st
     lib.solid_block_keys.argtypes = [vp, vp, vp]
     lib.solid_dump_ex.restype = st
+    lib.solid_block_table.restype = st
+    lib.solid_block_table.argtypes = [vp, vp, vp]
+    lib.solid_dump_phys.restype = st
+    lib.solid_dump_phys.argtypes = [vp, vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
     lib.solid_dump_ex.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
     for name in ["solid_reset", "solid_checkpoint", "solid_restore"]:
         getattr(lib, name).restype = st
@@ -174,14 +180,16 @@ class Index:
     def __init__(self, policy: str = "solidarity", capacity_blocks: int = 1 << 20,
                  max_batch_tokens: int = 1 << 24, max_batch_requests: int = 1 << 16,
                  max_blocks: int = 8192, seed: int = 0x5011D000, device: int = 0,
-                 world: int = 1, rank: int = 0, evict: bool = False, hash_components: int = 1):
+                 world: int = 1, rank: int = 0, evict: bool = False, hash_components: int = 1,
+                 block_table: bool = False):
         """evict=True: LRU eviction at capacity_blocks instead of
         SOLID_ERR_CAPACITY; lookup() then synchronises its stream.  hash_components=2: H-def v3
-        two-component keys."""
+        two-component keys.  block_table=True: physical KV block ids and
+        per-request block tables (admission synchronous)."""
         self.lib = load_library()
         cfg = _Config(16, max_blocks, capacity_blocks, max_batch_tokens, max_batch_requests,
                       seed & 0xFFFFFFFFFFFFFFFF, POLICY[policy], device, world, rank,
-                      1 if evict else 0, hash_components)
+                      1 if evict else 0, hash_components, 1 if block_table else 0)
         self.world, self.rank = world, rank
         h = ctypes.c_void_p()
         rc = self.lib.solid_init(ctypes.byref(cfg), ctypes.byref(h))
@@ -360,6 +368,28 @@ class Index:
         self._check(self.lib.solid_dump_ex(self.h, ctypes.c_void_p(out.ctypes.data), n.value,
                                            ctypes.byref(n)))
         return out[:int(n.value)]
+
+    def block_table(self, n_tokens: int, stream=None):
+        """Block table of the last committed batch (solid_block_table, R27): int32 tensor
+        [ceil(T/16)] (uint32 values; -1 = NONE), the physical block of request j's block b at
+        index offsets[j] // 16 + b.  Positions no full block covers keep -2."""
+        import torch
+        out = torch.full((max((n_tokens + 15) // 16, 1),), -2, dtype=torch.int32,
+                         device=torch.device("cuda", self.device))
+        self._check(self.lib.solid_block_table(self.h, ctypes.c_void_p(out.data_ptr()),
+                                               self._stream(stream)))
+        return out
+
+    def dump_phys(self):
+        """(keys uint64, physical blocks uint32) of the live entries, sorted by key."""
+        n = ctypes.c_uint64()
+        self._check(self.lib.solid_dump_phys(self.h, None, None, 0, ctypes.byref(n)))
+        m = int(n.value)
+        k = np.zeros(max(m, 1), dtype=np.uint64)
+        p = np.zeros(max(m, 1), dtype=np.uint32)
+        self._check(self.lib.solid_dump_phys(self.h, ctypes.c_void_p(k.ctypes.data),
+                                             ctypes.c_void_p(p.ctypes.data), m, ctypes.byref(n)))
+        return k[:m], p[:m]
 
     def reset(self):
         self._check(self.lib.solid_reset(self.h))

@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "solid.cu"), os.path.join(PKG, "csrc", "solid_activator.cu")]
 DEPS = SRC + [os.path.join(PKG, "csrc", "solid_math.cuh"), os.path.join(PKG, "csrc", "solid_dist.inc"),
-               os.path.join(PKG, "csrc", "solid_evict.inc"),
+               os.path.join(PKG, "csrc", "solid_evict.inc"), os.path.join(PKG, "csrc", "solid_pool.inc"),
                os.path.join(ROOT, "include", "solid.h")]
 LIB = os.path.join(PKG, "lib", "libsolid.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

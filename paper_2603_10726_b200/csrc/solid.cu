@@ -1271,6 +1271,7 @@ struct solid_ctx {
   uint64_t last_add = 0;
   // LRU eviction mode (solid_evict.inc)
   struct Evict* ev_state = nullptr;
+  struct Pool* pool = nullptr;     // block_table: physical blocks + block tables (solid_pool.inc)
   uint32_t* long_q = nullptr;      // K_A long-request queue (max_batch_requests entries)
 };
 
@@ -1316,9 +1317,18 @@ static solid_status evict_reset(solid_ctx* ctx, cudaStream_t s);
 static solid_status evict_scratch_reset(solid_ctx* ctx, cudaStream_t s);
 static solid_status evict_checkpoint(solid_ctx* ctx);
 static solid_status evict_restore(solid_ctx* ctx);
+static void pool_free(solid_ctx* ctx);
+static solid_status pool_init(solid_ctx* ctx);
+static solid_status pool_reset(solid_ctx* ctx, cudaStream_t s);
+static solid_status pool_pre(solid_ctx* ctx, cudaStream_t s, uint32_t tf);
+static solid_status pool_commit(solid_ctx* ctx, cudaStream_t s, uint32_t tf, uint64_t new_entries,
+                                uint64_t evicted, uint64_t ebound);
+static solid_status pool_checkpoint(solid_ctx* ctx);
+static solid_status pool_restore(solid_ctx* ctx);
 
 static void free_all(solid_ctx* c) {
   evict_free(c);
+  pool_free(c);
   cudaFree(c->tab);
   cudaFree(c->tab_ckpt);
   cudaFree(c->stab);
@@ -1387,6 +1397,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   if (cfg->evict > 1 || (cfg->evict && (world != 1 || cfg->capacity_blocks < cfg->max_blocks)))
     return SOLID_ERR_INVALID;
   if (cfg->hash_components > 2) return SOLID_ERR_INVALID;
+  if (cfg->block_table > 1 || (cfg->block_table && world != 1)) return SOLID_ERR_INVALID;
   ctx = new solid_ctx();
   ctx->cfg = *cfg;
   ctx->cfg.world = world;
@@ -1479,6 +1490,14 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   set_slot(ctx, 0);
   if (cfg->evict) {
     rc = evict_init(ctx);
+    if (rc != SOLID_OK) {
+      free_all(ctx);
+      delete ctx;
+      return rc;
+    }
+  }
+  if (cfg->block_table) {
+    rc = pool_init(ctx);
     if (rc != SOLID_OK) {
       free_all(ctx);
       delete ctx;
@@ -1703,6 +1722,11 @@ static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, boo
     CK(cudaStreamSynchronize(s));
     return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9)");
   }
+  if (ctx->pool && current && !async_mode) {   // physical blocks (solid_pool.inc)
+    solid_status rc = pool_commit(ctx, s, ctx->cfg.policy == SOLID_POLICY_SOLIDARITY ? h.conv : 0u,
+                                  h.new_entries, 0, 0);
+    if (rc != SOLID_OK) return rc;
+  }
   solid_stats_t& S = ctx->stats;
   ctx->rounds = (ctx->cfg.policy == SOLID_POLICY_SOLIDARITY) ? h.conv : (n ? 1u : 0u);
   if (current) {
@@ -1767,6 +1791,8 @@ extern "C" solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* bat
   if (!ctx) return SOLID_ERR_INVALID;
   if (ctx->ev_state)
     return fail(ctx, SOLID_ERR_STATE, "evict mode: admission is synchronous (lookup + insert)");
+  if (ctx->pool)
+    return fail(ctx, SOLID_ERR_STATE, "block_table: admission is synchronous (lookup + insert)");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "admit_batch with a pending lookup");
   if (ctx->outstanding == kRing)
     return fail(ctx, SOLID_ERR_STATE,
@@ -1854,7 +1880,7 @@ static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* to
   // Large batches are admitted as kHostChunks consecutive sub-batches (identical results,
   // reading R1) so the token copy of chunk k+1 (copy stream) overlaps the admission of chunk k.
   const uint32_t K = (T * (uint64_t)token_bytes >= (64ull << 20) && n >= 4 * kHostChunks &&
-                      !ctx->ev_state) ? kHostChunks : 1u;
+                      !ctx->ev_state && !ctx->pool) ? kHostChunks : 1u;
   if (K > 1 && !ctx->s_copy) {
     CK(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
     for (auto& e : ctx->ev_chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -2041,6 +2067,10 @@ extern "C" solid_status solid_reset(solid_ctx* ctx) {
     solid_status rc = evict_reset(ctx, s);
     if (rc != SOLID_OK) return rc;
   }
+  if (ctx->pool) {
+    solid_status rc = pool_reset(ctx, s);
+    if (rc != SOLID_OK) return rc;
+  }
   CK(cudaMemsetAsync(ctx->live_dev, 0, sizeof(unsigned long long), s));
   if (!ctx->outstanding) CK(cudaStreamSynchronize(s));
   if (ctx->poisoned) ctx->head = ctx->outstanding = 0;   // their results are lost with the state
@@ -2060,6 +2090,10 @@ extern "C" solid_status solid_checkpoint(solid_ctx* ctx) {
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
   ctx->live_ckpt = ctx->live;
+  if (ctx->pool) {
+    solid_status rc = pool_checkpoint(ctx);
+    if (rc != SOLID_OK) return rc;
+  }
   if (ctx->ev_state) return evict_checkpoint(ctx);
   if (!ctx->tab_ckpt) CK(cudaMalloc(&ctx->tab_ckpt, ctx->tcap * sizeof(ulonglong2)));
   CK(cudaMemcpy(ctx->tab_ckpt, ctx->tab, ctx->tcap * sizeof(ulonglong2), cudaMemcpyDeviceToDevice));
@@ -2075,6 +2109,10 @@ extern "C" solid_status solid_restore(solid_ctx* ctx) {
   if (rc0 != SOLID_OK) return rc0;
   CK(cudaSetDevice(ctx->dev));
   if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->pool) {
+    solid_status rc = pool_restore(ctx);
+    if (rc != SOLID_OK) return rc;
+  }
   if (ctx->ev_state) {
     solid_status rc = evict_restore(ctx);
     if (rc != SOLID_OK) return rc;
@@ -2088,5 +2126,20 @@ extern "C" solid_status solid_restore(solid_ctx* ctx) {
   return SOLID_OK;
 }
 
+namespace solid {
+// runs f with the policy as a compile-time constant
+template <typename F>
+static void by_policy(int policy, F&& f) {
+  switch (policy) {
+    case SOLID_POLICY_APC: f(std::integral_constant<int, SOLID_POLICY_APC>()); break;
+    case SOLID_POLICY_USER_ISOLATION:
+      f(std::integral_constant<int, SOLID_POLICY_USER_ISOLATION>()); break;
+    default: f(std::integral_constant<int, SOLID_POLICY_SOLIDARITY>()); break;
+  }
+}
+
+}  // namespace solid
+
 #include "solid_dist.inc"
+#include "solid_pool.inc"
 #include "solid_evict.inc"

@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import bench
 ap = argparse.ArgumentParser()
-ap.add_argument("part", choices=["evict", "policy", "hash2", "configs"])
+ap.add_argument("part", choices=["evict", "policy", "hash2", "configs", "btab"])
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--no-cpu", action="store_true")
@@ -22,5 +22,6 @@ elif a.part == "policy":
 else:
     import paper_2603_10726_b200 as P
     s, _ = bench._workload("c2", 0)
-    r = bench.measure_hash2(dev, a, P.to_device(s, dev), s)
+    fn = bench.measure_hash2 if a.part == "hash2" else bench.measure_block_table
+    r = fn(dev, a, P.to_device(s, dev), s)
 print(json.dumps(r, indent=1))
