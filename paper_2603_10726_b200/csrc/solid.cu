@@ -45,6 +45,7 @@ struct alignas(128) SegCounter {       // one id counter per 128-byte line: atom
 constexpr uint32_t kSubSnap = 4095;
 constexpr uint32_t kLongBlocks = 128;   // K_A: longer requests are hashed by a whole CTA
 constexpr uint64_t kLongMaxBatch = 148 * 32;   // ... in batches of at most this many requests
+constexpr int kIsoG = 4;                         // resolver: isolated-walk groups in flight
 constexpr uint32_t kMaxRounds = 4093;
 constexpr uint32_t kMaxEpoch = (0xFFFFFFFFu / 4096u) - 1;
 
@@ -791,15 +792,38 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
       // same divert depth as last round: the isolated keys of blocks f..n-1 are registered and
       // their ids cached in iso_id[] (created in an earlier round, so the staged state already
       // carries their index snapshot); the first group was prefetched above
-      for (uint32_t g = (uint32_t)f; g < n; g += 32) {
-        const uint32_t i = g + lane;
-        bool vis = false;
-        if (g == (uint32_t)f) vis = i < n && iso_pre_vis;
-        else if (i < n) vis = iso_visible(kp, iso_ids[i], R, limR, limW);
-        const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
-        if (inv) {
-          m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
-          break;
+      // kIsoG groups with their id and state loads in flight together (long isolated walks)
+      bool stop = false;
+      for (uint32_t g0 = (uint32_t)f; g0 < n && !stop; g0 += 32 * kIsoG) {
+        uint32_t idv[kIsoG];
+        unsigned long long va[kIsoG], vb[kIsoG];
+#pragma unroll
+        for (int q = 0; q < kIsoG; ++q) {
+          const uint32_t i = g0 + 32 * q + lane;
+          idv[q] = (i < n && !(q == 0 && g0 == (uint32_t)f)) ? iso_ids[i] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kIsoG; ++q) {
+          va[q] = vb[q] = ~0ull;
+          if (idv[q]) {
+            const Hot* h = kp.hot + idv[q];
+            va[q] = ldw64(&h->v[2 * R]);
+            vb[q] = ldw64(&h->v[2 - 2 * R]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kIsoG; ++q) {
+          const uint32_t g = g0 + 32 * q;
+          if (g >= n) break;
+          const uint32_t i = g + lane;
+          const bool vis = (q == 0 && g0 == (uint32_t)f) ? (i < n && iso_pre_vis)
+                                                          : (idv[q] && (va[q] < limR || vb[q] < limW));
+          const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
+          if (inv) {
+            m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
+            stop = true;
+            break;
+          }
         }
       }
     } else {

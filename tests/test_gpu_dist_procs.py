@@ -22,7 +22,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, outdir):
+def _worker(rank, world, port, name, outdir, nc=1):
     import torch
     import torch.distributed as dist
     import paper_2603_10726_b200 as P
@@ -35,7 +35,8 @@ def _worker(rank, world, port, name, outdir):
     lo, hi = n * rank // world, n * (rank + 1) // world
     part = s.slice(lo, hi)
     shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(4 * s.n_blocks(), 4096),
-                         max_batch_tokens=s.n_tokens + 64, max_batch_requests=n, seed=SEED)
+                         max_batch_tokens=s.n_tokens + 64, max_batch_requests=n, seed=SEED,
+                         hash_components=nc)
     ex = TorchExchange(shard, staging=True)
     d = P.to_device(part)
     res, rounds = ex.admit(d["tokens"], d["offsets"], d["users"], d["enforce"], seq_base=lo)
@@ -46,13 +47,15 @@ def _worker(rank, world, port, name, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["c1", "c2_small"])
-def test_two_ranks_gloo_staging(name, tmp_path):
+@pytest.mark.parametrize("name,nc", [("c1", 1), ("c2_small", 1), ("c2_small", 2)])
+def test_two_ranks_gloo_staging(name, nc, tmp_path):
+    """nc = 2: H-def v3 two-component keys across real ranks."""
     import torch.multiprocessing as mp
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path), nc), nprocs=world,
+             join=True)
     s = c1_tiny() if name == "c1" else c2_shared_prompt(users=30, reqs_per_user=10)
-    o = Oracle(16, SEED, 2)
+    o = Oracle(16, SEED, 2, components=nc)
     exp = o.process(s)
     got = np.concatenate([np.load(tmp_path / f"res{r}.npy") for r in range(world)])
     assert np.array_equal(got, exp)
