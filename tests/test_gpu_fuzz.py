@@ -65,3 +65,47 @@ def test_fuzz(chunk):
         for f in ed.dtype.names:
             assert np.array_equal(gd[f], ed[f]), (ctx, f)
         idx.close()
+
+
+def _admit_bt(P, idx, o, b, evict, ctx):
+    """Admit with splitting; the oracle takes the same sub-batches; every accepted sub-batch's
+    block table (covered positions) must equal the oracle's."""
+    import torch
+    try:
+        got = P.as_numpy(idx.admit(**P.to_device(b)))
+        torch.cuda.synchronize()
+    except P.SolidError as e:
+        if not evict or e.status != P.SOLID_ERR_CAPACITY or b.n_requests < 2:
+            raise
+        h = b.n_requests // 2
+        _admit_bt(P, idx, o, b.slice(0, h), evict, ctx)
+        _admit_bt(P, idx, o, b.slice(h, b.n_requests), evict, ctx)
+        return
+    assert np.array_equal(got, o.process(b)), ctx
+    if b.n_requests:
+        bt = idx.block_table(b.n_tokens).cpu().numpy().view(np.uint32)
+        ob, offs = o.block_table(), b.offsets.astype(np.int64)
+        for j in range(b.n_requests):
+            a, n = offs[j] // 16, (offs[j + 1] - offs[j]) // 16
+            assert np.array_equal(bt[a:a + n], ob[a:a + n]), (ctx, j)
+
+
+@pytest.mark.parametrize("chunk", range(int(os.environ.get("FUZZ_CHUNKS", "4")) // 2 or 1))
+def test_fuzz_block_tables(chunk):
+    """The same random cases with physical block ids on: every block table and every live
+    entry's block equal the oracle's FIFO pool (R26-R28)."""
+    import paper_2603_10726_b200 as P
+    for seed in range(10_000 + chunk * 40, 10_000 + chunk * 40 + 40):
+        s, policy, evict, cap, nc, cuts = _case(seed)
+        idx = P.Index(policy, capacity_blocks=cap, max_batch_tokens=max(s.n_tokens, 64) + 64,
+                      max_batch_requests=max(s.n_requests, 1), max_blocks=8, seed=SEED,
+                      evict=evict, hash_components=nc, block_table=True)
+        o = Oracle(16, SEED, POLS.index(policy), capacity=cap if evict else 0, components=nc,
+                   pool=cap)
+        ctx = (seed, policy, evict, cap, nc)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            _admit_bt(P, idx, o, s.slice(a, b), evict, ctx)
+        gk, gp = idx.dump_phys()
+        ek, ep = o.dump_phys()
+        assert np.array_equal(gk, ek) and np.array_equal(gp, ep), ctx
+        idx.close()
