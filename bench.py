@@ -511,7 +511,7 @@ def run_sharded(args, world, rank, local):
     import torch
     import torch.distributed as dist
     import paper_2603_10726_b200 as P
-    from paper_2603_10726_b200.dist import ShardedIndex, TorchExchange, run_protocol
+    from paper_2603_10726_b200.dist import PeerExchange, ShardedIndex, TorchExchange, run_protocol
     from workloads import c2_shared_prompt
 
     per = 100_000 if args.config == "c2" else 10_000
@@ -524,7 +524,16 @@ def run_sharded(args, world, rank, local):
     shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
                          max_batch_tokens=s.n_tokens + 64, max_batch_requests=per, seed=SEED,
                          device=local)
-    ex = TorchExchange(shard, staging=os.environ.get("SOLID_DIST_BACKEND", "nccl") != "nccl")
+    # SOLID_DIST_EXCHANGE=p2p: the library's own exchange over peer memory;
+    # default: torch.distributed (NCCL, or gloo with host staging)
+    xport = os.environ.get("SOLID_DIST_EXCHANGE", "torch")
+    if xport == "p2p":
+        ex = PeerExchange(shard)
+        xname = "p2p (CUDA IPC peer stores + mailbox flags)"
+    else:
+        staging = os.environ.get("SOLID_DIST_BACKEND", "nccl") != "nccl"
+        ex = TorchExchange(shard, staging=staging)
+        xname = "gloo, host-staged" if staging else "nccl all_to_all + batched p2p"
     coll = {"s": 0.0}
 
     def timed_exchange(counts, flags=None):
@@ -600,7 +609,8 @@ def run_sharded(args, world, rank, local):
             "config": {"workload": f"c2_shared_prompt x{world}: {users} users x 100 requests, "
                                    f"2000-token prompts, {per} requests per GPU",
                        "policy": "solidarity", "parallelism": f"key-hash-sharded index over "
-                       f"{world} GPUs, NCCL exchange per resolver round",
+                       f"{world} GPUs, record exchange per resolver round",
+                       "exchange": xname,
                        "l2": "inputs larger than L2", "restore": "index reset before each step"},
             "roofline": {"bound": "hbm", "kernel": "whole sharded step (per GPU)",
                          "achieved": alg / world / (tot_ms / args.steps / 1e3) / 1e9,

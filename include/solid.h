@@ -330,6 +330,24 @@ solid_status solid_dist_round(solid_ctx* ctx, uint32_t t, const uint64_t* recv_c
                               uint32_t* changed, void* stream);
 solid_status solid_dist_commit(solid_ctx* ctx, int mode, uint64_t* new_entries, void* stream);
 
+/* ---- Peer-memory exchange for the sharded index ---------------------------
+ * Replaces the caller-driven all-to-all-v: each rank exports a ctx-owned device region (mailbox +
+ * two receive buffers) as a CUDA IPC handle, every rank maps every peer's region, and one
+ * solid_dist_p2p_exchange moves the last pack's records straight into the peers' receive
+ * buffers (NVLink / NVSwitch peer stores) and signals them through the mailbox — one push and
+ * one wait kernel, no collective library.  All ranks must be processes on one node. */
+/* 64-byte cudaIpcMemHandle_t of this shard's region into handle_out (allocated on first call). */
+solid_status solid_dist_p2p_export(solid_ctx* ctx, void* handle_out);
+/* Map the peers' regions; handles = world x 64 bytes in rank order (own entry ignored).  Every
+ * rank must have exported first (the caller all-gathers the handles). */
+solid_status solid_dist_p2p_connect(solid_ctx* ctx, const void* handles);
+/* Exchange the last pack (the counts of solid_dist_counts): recv_counts_out[world] = records
+ * received from each source, ready for the next solid_dist_owner_ingest / solid_dist_round;
+ * flag = this rank's "decision changed" bit, *gflag_out (may be NULL) = max over all ranks.
+ * Every rank must call it the same number of times.  Synchronises `stream`. */
+solid_status solid_dist_p2p_exchange(solid_ctx* ctx, uint32_t flag, uint64_t* recv_counts_out,
+                                     uint32_t* gflag_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

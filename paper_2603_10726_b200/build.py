@@ -10,6 +10,7 @@ ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "solid.cu"), os.path.join(PKG, "csrc", "solid_activator.cu")]
 DEPS = SRC + [os.path.join(PKG, "csrc", "solid_math.cuh"), os.path.join(PKG, "csrc", "solid_dist.inc"),
                os.path.join(PKG, "csrc", "solid_evict.inc"), os.path.join(PKG, "csrc", "solid_pool.inc"),
+               os.path.join(PKG, "csrc", "solid_p2p.inc"),
                os.path.join(ROOT, "include", "solid.h")]
 LIB = os.path.join(PKG, "lib", "libsolid.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

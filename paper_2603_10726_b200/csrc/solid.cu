@@ -1292,6 +1292,7 @@ struct solid_ctx {
   uint64_t gen = 0;                         // reset generation
   // sharded mode (solid_dist.inc)
   struct Dist* dist = nullptr;
+  struct P2P* p2p = nullptr;       // sharded: peer-memory exchange (solid_p2p.inc)
   uint64_t last_add = 0;
   // LRU eviction mode (solid_evict.inc)
   struct Evict* ev_state = nullptr;
@@ -1342,6 +1343,7 @@ static solid_status evict_scratch_reset(solid_ctx* ctx, cudaStream_t s);
 static solid_status evict_checkpoint(solid_ctx* ctx);
 static solid_status evict_restore(solid_ctx* ctx);
 static void pool_free(solid_ctx* ctx);
+static void p2p_free(solid_ctx* ctx);
 static solid_status pool_init(solid_ctx* ctx);
 static solid_status pool_reset(solid_ctx* ctx, cudaStream_t s);
 static solid_status pool_pre(solid_ctx* ctx, cudaStream_t s, uint32_t tf);
@@ -1351,6 +1353,7 @@ static solid_status pool_checkpoint(solid_ctx* ctx);
 static solid_status pool_restore(solid_ctx* ctx);
 
 static void free_all(solid_ctx* c) {
+  p2p_free(c);
   evict_free(c);
   pool_free(c);
   cudaFree(c->tab);
@@ -1546,6 +1549,7 @@ extern "C" solid_status solid_destroy(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
   cudaSetDevice(ctx->dev);
   cudaDeviceSynchronize();
+  p2p_free(ctx);
   dist_free(ctx);
   free_all(ctx);
   delete ctx;
@@ -2165,5 +2169,6 @@ static void by_policy(int policy, F&& f) {
 }  // namespace solid
 
 #include "solid_dist.inc"
+#include "solid_p2p.inc"
 #include "solid_pool.inc"
 #include "solid_evict.inc"

@@ -158,6 +158,55 @@ def loopback_admit(shards: List[ShardedIndex], local_batches, seq_bases):
     return run_protocol(shards, args, exchange, lambda xs: max(xs))
 
 
+class PeerExchange:
+    """One shard per process on one node, records moved by the library itself over peer memory
+    (solid_dist_p2p_*: CUDA IPC-mapped receive buffers, NVLink / NVSwitch stores, mailbox flags;
+    DESIGN.md §7.4).  torch.distributed (any backend) only all-gathers the 64-byte handles once
+    and takes the per-batch overflow vote."""
+
+    def __init__(self, shard: ShardedIndex, group=None):
+        import torch.distributed as dist
+        self.shard, self.group = shard, group
+        lib, h = shard.index.lib, shard.index.h
+        lib.solid_dist_p2p_export.restype = ctypes.c_int
+        lib.solid_dist_p2p_export.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        lib.solid_dist_p2p_connect.restype = ctypes.c_int
+        lib.solid_dist_p2p_connect.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        lib.solid_dist_p2p_exchange.restype = ctypes.c_int
+        lib.solid_dist_p2p_exchange.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_void_p]
+        mine = ctypes.create_string_buffer(64)
+        shard.index._check(lib.solid_dist_p2p_export(h, mine))
+        allh = [None] * shard.world
+        dist.all_gather_object(allh, bytes(mine.raw), group=self.group)
+        table = ctypes.create_string_buffer(b"".join(allh), 64 * shard.world)
+        shard.index._check(lib.solid_dist_p2p_connect(h, table))
+        dist.barrier(group=self.group)
+
+    def exchange(self, send_counts_list, flags=None):
+        sh = self.shard
+        rc = (ctypes.c_uint64 * sh.world)()
+        g = ctypes.c_uint32()
+        sh.index._check(sh.index.lib.solid_dist_p2p_exchange(
+            sh.index.h, 1 if flags and flags[0] else 0, rc, ctypes.byref(g), Index._stream(None)))
+        recv = np.array(list(rc), dtype=np.int64)
+        return [recv] if flags is None else ([recv], int(g.value))
+
+    def allreduce_max(self, xs):
+        import torch
+        import torch.distributed as dist
+        v = torch.tensor([max(xs)], dtype=torch.int64)
+        if dist.get_backend(self.group) == "nccl":
+            v = v.to(self.shard.send.device)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX, group=self.group)
+        return int(v.item())
+
+    def admit(self, tokens, offsets, users, enforce=None, seq_base: int = 0):
+        res, rounds = run_protocol([self.shard], [(tokens, offsets, users, enforce, seq_base)],
+                                   self.exchange, self.allreduce_max)
+        return res[0], rounds
+
+
 class TorchExchange:
     """One shard per rank of a torch.distributed process group (NCCL for CUDA buffers).
 

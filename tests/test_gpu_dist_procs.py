@@ -63,3 +63,50 @@ def test_two_ranks_gloo_staging(name, nc, tmp_path):
     dumps = dumps[np.argsort(dumps["key"])]
     ed = o.dump()
     assert all(np.array_equal(dumps[f], ed[f]) for f in ["key", "owner", "sharer"])
+
+
+def _p2p_worker(rank, world, port, name, outdir, nc):
+    import torch
+    import torch.distributed as dist
+    import paper_2603_10726_b200 as P
+    from paper_2603_10726_b200.dist import PeerExchange, ShardedIndex
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    s = c1_tiny() if name == "c1" else c2_shared_prompt(users=30, reqs_per_user=10)
+    n = s.n_requests
+    shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(4 * s.n_blocks(), 4096),
+                         max_batch_tokens=s.n_tokens + 64, max_batch_requests=n, seed=SEED,
+                         hash_components=nc)
+    ex = PeerExchange(shard)
+    # two batches: the second finds the first's entries on their owners
+    for k, (a, b) in enumerate([(0, n // 2), (n // 2, n)]):
+        lo = a + (b - a) * rank // world
+        hi = a + (b - a) * (rank + 1) // world
+        d = P.to_device(s.slice(lo, hi))
+        res, rounds = ex.admit(d["tokens"], d["offsets"], d["users"], d["enforce"], seq_base=lo)
+        torch.cuda.synchronize()
+        np.save(os.path.join(outdir, f"res{k}_{rank}.npy"), P.as_numpy(res))
+    np.save(os.path.join(outdir, f"dump{rank}.npy"), shard.index.dump())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,nc,world", [("c1", 1, 2), ("c2_small", 1, 2), ("c2_small", 2, 3)])
+def test_ranks_peer_memory_exchange(name, nc, world, tmp_path):
+    """The library's own exchange over CUDA IPC peer memory (solid_dist_p2p_*):
+    2-3 processes (sharing this box's GPU: IPC-mapped buffers of one device), two batches."""
+    import torch.multiprocessing as mp
+    mp.spawn(_p2p_worker, args=(world, _free_port(), name, str(tmp_path), nc), nprocs=world,
+             join=True)
+    s = c1_tiny() if name == "c1" else c2_shared_prompt(users=30, reqs_per_user=10)
+    n = s.n_requests
+    o = Oracle(16, SEED, 2, components=nc)
+    for k, (a, b) in enumerate([(0, n // 2), (n // 2, n)]):
+        exp = o.process(s.slice(a, b))
+        got = np.concatenate([np.load(tmp_path / f"res{k}_{r}.npy") for r in range(world)])
+        assert np.array_equal(got, exp), k
+    dumps = np.concatenate([np.load(tmp_path / f"dump{r}.npy") for r in range(world)])
+    dumps = dumps[np.argsort(dumps["key"])]
+    ed = o.dump()
+    assert all(np.array_equal(dumps[f], ed[f]) for f in ["key", "owner", "sharer"])
