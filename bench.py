@@ -511,7 +511,8 @@ def run_sharded(args, world, rank, local):
     import torch
     import torch.distributed as dist
     import paper_2603_10726_b200 as P
-    from paper_2603_10726_b200.dist import PeerExchange, ShardedIndex, TorchExchange, run_protocol
+    from paper_2603_10726_b200.dist import (PeerExchange, ShardedIndex, TorchExchange, run_protocol,
+                                            run_protocol_device)
     from workloads import c2_shared_prompt
 
     per = 100_000 if args.config == "c2" else 10_000
@@ -527,9 +528,10 @@ def run_sharded(args, world, rank, local):
     # SOLID_DIST_EXCHANGE=p2p: the library's own exchange over peer memory;
     # default: torch.distributed (NCCL, or gloo with host staging)
     xport = os.environ.get("SOLID_DIST_EXCHANGE", "torch")
-    if xport == "p2p":
-        ex = PeerExchange(shard)
-        xname = "p2p (CUDA IPC peer stores + mailbox flags)"
+    if xport in ("p2p", "p2p-dev"):
+        ex = PeerExchange(shard, device_counts=xport == "p2p-dev")
+        xname = "p2p (CUDA IPC peer stores + mailbox flags)" + (
+            ", device-resident counts" if xport == "p2p-dev" else "")
     else:
         staging = os.environ.get("SOLID_DIST_BACKEND", "nccl") != "nccl"
         ex = TorchExchange(shard, staging=staging)
@@ -543,7 +545,16 @@ def run_sharded(args, world, rank, local):
         coll["s"] += time.perf_counter() - t0
         return r
 
+    def timed_exchange_dev(sync):
+        t0 = time.perf_counter()
+        r = ex.exchange_dev(sync)
+        coll["s"] += time.perf_counter() - t0     # host time of the enqueue (+ wait if sync)
+        return r
+
     def step():
+        if xport == "p2p-dev":
+            return run_protocol_device(shard, (d["tokens"], d["offsets"], d["users"], None, lo),
+                                       timed_exchange_dev, ex.allreduce_max)
         res, t = run_protocol([shard], [(d["tokens"], d["offsets"], d["users"], None, lo)],
                               timed_exchange, ex.allreduce_max)
         return res[0], t
@@ -591,7 +602,7 @@ def run_sharded(args, world, rank, local):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             dt, do, du = ht.to(dev, non_blocking=True), ho.to(dev, non_blocking=True), hu.to(dev, non_blocking=True)
-            r, _ = run_protocol([shard], [(dt, do, du, None, lo)], ex.exchange, ex.allreduce_max)
+            r = [ex.admit(dt, do, du, None, lo)[0]]
             r[0].cpu()
             et += time.perf_counter() - t0
         tt = torch.tensor([et], dtype=torch.float64, device=dev)

@@ -347,6 +347,16 @@ solid_status solid_dist_p2p_connect(solid_ctx* ctx, const void* handles);
  * Every rank must call it the same number of times.  Synchronises `stream`. */
 solid_status solid_dist_p2p_exchange(solid_ctx* ctx, uint32_t flag, uint64_t* recv_counts_out,
                                      uint32_t* gflag_out, void* stream);
+/* Device-counts mode (on = 1; between batches, after connect): solid_dist_owner_ingest and
+ * solid_dist_round then accept recv_counts = NULL and no longer synchronise (their send counts
+ * and errors stay on the device); solid_dist_p2p_exchange_dev moves the last pack reading its
+ * counts — and, after a round, that round's changed flag — on the device, and writes the
+ * received counts straight into the next call's input.  sync = 1: wait for the stream, return
+ * the global changed flag in *gflag_out and report a batch error (use it for each round's INT
+ * exchange); sync = 0: fully asynchronous (REG / PULL).  solid_dist_commit checks errors. */
+solid_status solid_dist_p2p_device_counts(solid_ctx* ctx, uint32_t on);
+solid_status solid_dist_p2p_exchange_dev(solid_ctx* ctx, uint32_t sync, uint32_t* gflag_out,
+                                         void* stream);
 
 #ifdef __cplusplus
 }

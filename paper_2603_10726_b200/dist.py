@@ -80,15 +80,18 @@ class ShardedIndex:
         return self.counts()
 
     def owner_ingest(self, phase: int, recv_counts, stream=None):
+        """recv_counts None: device-resident counts (peer-memory exchange, device-counts mode)."""
+        rc = None if recv_counts is None else self._u64arr(recv_counts)
         self.index._check(self.index.lib.solid_dist_owner_ingest(
-            self.index.h, phase, self._u64arr(recv_counts), Index._stream(stream)))
-        return self.counts()
+            self.index.h, phase, rc, Index._stream(stream)))
+        return None if recv_counts is None else self.counts()
 
     def round(self, t: int, recv_counts, stream=None):
         ch = ctypes.c_uint32()
+        rc = None if recv_counts is None else self._u64arr(recv_counts)
         self.index._check(self.index.lib.solid_dist_round(
-            self.index.h, t, self._u64arr(recv_counts), ctypes.byref(ch), Index._stream(stream)))
-        return self.counts(), int(ch.value)
+            self.index.h, t, rc, ctypes.byref(ch), Index._stream(stream)))
+        return (None if recv_counts is None else self.counts()), int(ch.value)
 
     def commit(self, mode: int, stream=None):
         add = ctypes.c_uint64()
@@ -164,9 +167,11 @@ class PeerExchange:
     DESIGN.md §7.4).  torch.distributed (any backend) only all-gathers the 64-byte handles once
     and takes the per-batch overflow vote."""
 
-    def __init__(self, shard: ShardedIndex, group=None):
+    def __init__(self, shard: ShardedIndex, group=None, device_counts: bool = False):
+        """device_counts=True: counts stay on the device and only the INT exchange of each
+        round synchronises the host (for the stop decision) — see admit()."""
         import torch.distributed as dist
-        self.shard, self.group = shard, group
+        self.shard, self.group, self.device_counts = shard, group, device_counts
         lib, h = shard.index.lib, shard.index.h
         lib.solid_dist_p2p_export.restype = ctypes.c_int
         lib.solid_dist_p2p_export.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
@@ -181,6 +186,12 @@ class PeerExchange:
         dist.all_gather_object(allh, bytes(mine.raw), group=self.group)
         table = ctypes.create_string_buffer(b"".join(allh), 64 * shard.world)
         shard.index._check(lib.solid_dist_p2p_connect(h, table))
+        lib.solid_dist_p2p_device_counts.restype = ctypes.c_int
+        lib.solid_dist_p2p_device_counts.argtypes = [ctypes.c_void_p, ctypes.c_uint32]
+        lib.solid_dist_p2p_exchange_dev.restype = ctypes.c_int
+        lib.solid_dist_p2p_exchange_dev.argtypes = [ctypes.c_void_p, ctypes.c_uint32,
+                                                    ctypes.c_void_p, ctypes.c_void_p]
+        shard.index._check(lib.solid_dist_p2p_device_counts(h, 1 if device_counts else 0))
         dist.barrier(group=self.group)
 
     def exchange(self, send_counts_list, flags=None):
@@ -201,10 +212,45 @@ class PeerExchange:
         dist.all_reduce(v, op=dist.ReduceOp.MAX, group=self.group)
         return int(v.item())
 
+    def exchange_dev(self, sync: bool) -> int:
+        sh = self.shard
+        g = ctypes.c_uint32()
+        sh.index._check(sh.index.lib.solid_dist_p2p_exchange_dev(
+            sh.index.h, 1 if sync else 0, ctypes.byref(g), Index._stream(None)))
+        return int(g.value)
+
     def admit(self, tokens, offsets, users, enforce=None, seq_base: int = 0):
-        res, rounds = run_protocol([self.shard], [(tokens, offsets, users, enforce, seq_base)],
-                                   self.exchange, self.allreduce_max)
-        return res[0], rounds
+        if not self.device_counts:
+            res, rounds = run_protocol([self.shard], [(tokens, offsets, users, enforce, seq_base)],
+                                       self.exchange, self.allreduce_max)
+            return res[0], rounds
+        return run_protocol_device(self.shard, (tokens, offsets, users, enforce, seq_base),
+                                   self.exchange_dev, self.allreduce_max)
+
+
+def run_protocol_device(shard: ShardedIndex, begin_args, exchange_dev, allreduce_max):
+    """The protocol of run_protocol with device-resident counts (peer-memory exchange): the
+    host only waits at each round's INT exchange (stop decision) and at the commit."""
+    shard.begin(*begin_args)
+    exchange_dev(False)                                           # REG
+    shard.owner_ingest(0, None)
+    exchange_dev(False)                                           # PULL
+    t = 1
+    while True:
+        shard.round(t, None)
+        changed = exchange_dev(True)                              # INT (+ changed)
+        shard.owner_ingest(t, None)
+        if shard.policy != "solidarity" or (t >= 2 and not changed):
+            break
+        exchange_dev(False)                                       # PULL
+        t += 1
+        if t > 4093:
+            raise SolidError(3, "sharded resolver did not converge")
+    rc = shard.commit(1)[0]
+    if allreduce_max([int(rc == SOLID_ERR_CAPACITY)]):
+        shard.commit(2)
+        raise SolidError(SOLID_ERR_CAPACITY, "index shard capacity exceeded; batch rolled back")
+    return shard.results(), t
 
 
 class TorchExchange:

@@ -65,7 +65,7 @@ def test_two_ranks_gloo_staging(name, nc, tmp_path):
     assert all(np.array_equal(dumps[f], ed[f]) for f in ["key", "owner", "sharer"])
 
 
-def _p2p_worker(rank, world, port, name, outdir, nc):
+def _p2p_worker(rank, world, port, name, outdir, nc, dc=False):
     import torch
     import torch.distributed as dist
     import paper_2603_10726_b200 as P
@@ -78,7 +78,7 @@ def _p2p_worker(rank, world, port, name, outdir, nc):
     shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(4 * s.n_blocks(), 4096),
                          max_batch_tokens=s.n_tokens + 64, max_batch_requests=n, seed=SEED,
                          hash_components=nc)
-    ex = PeerExchange(shard)
+    ex = PeerExchange(shard, device_counts=dc)
     # two batches: the second finds the first's entries on their owners
     for k, (a, b) in enumerate([(0, n // 2), (n // 2, n)]):
         lo = a + (b - a) * rank // world
@@ -92,12 +92,15 @@ def _p2p_worker(rank, world, port, name, outdir, nc):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,nc,world", [("c1", 1, 2), ("c2_small", 1, 2), ("c2_small", 2, 3)])
-def test_ranks_peer_memory_exchange(name, nc, world, tmp_path):
+@pytest.mark.parametrize("name,nc,world,dc", [("c1", 1, 2, False), ("c2_small", 1, 2, False),
+                                              ("c2_small", 2, 3, False), ("c1", 1, 2, True),
+                                              ("c2_small", 1, 3, True)])
+def test_ranks_peer_memory_exchange(name, nc, world, dc, tmp_path):
     """The library's own exchange over CUDA IPC peer memory (solid_dist_p2p_*):
-    2-3 processes (sharing this box's GPU: IPC-mapped buffers of one device), two batches."""
+    2-3 processes (sharing this box's GPU: IPC-mapped buffers of one device), two batches;
+    dc: device-resident counts (one host wait per round)."""
     import torch.multiprocessing as mp
-    mp.spawn(_p2p_worker, args=(world, _free_port(), name, str(tmp_path), nc), nprocs=world,
+    mp.spawn(_p2p_worker, args=(world, _free_port(), name, str(tmp_path), nc, dc), nprocs=world,
              join=True)
     s = c1_tiny() if name == "c1" else c2_shared_prompt(users=30, reqs_per_user=10)
     n = s.n_requests
