@@ -1344,6 +1344,7 @@ static solid_status evict_checkpoint(solid_ctx* ctx);
 static solid_status evict_restore(solid_ctx* ctx);
 static void pool_free(solid_ctx* ctx);
 static void p2p_free(solid_ctx* ctx);
+static void p2p_direct_targets(solid_ctx* ctx);
 static solid_status pool_init(solid_ctx* ctx);
 static solid_status pool_reset(solid_ctx* ctx, cudaStream_t s);
 static solid_status pool_pre(solid_ctx* ctx, cudaStream_t s, uint32_t tf);
