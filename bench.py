@@ -505,14 +505,14 @@ def run_sharded(args, world, rank, local):
     """N > 1: one key-hash-sharded index over all ranks.  The global batch is the
     C2 shape scaled by N (N x 1000 users sharing the system prompt, N x 100 000 requests, one
     seeded shuffle); rank r admits its contiguous slice; keys live on their owner shard; the
-    REG / PULL / INT records move over NCCL each resolver round.  Weak scaling: fixed requests
+    REG / PULL / INT records move each resolver round (peer memory, or NCCL).  Weak scaling: fixed requests
     per GPU.  Collectives are timed separately (host clock around the exchange calls, after a
     stream sync; the step itself by CUDA events, max over ranks)."""
     import torch
     import torch.distributed as dist
     import paper_2603_10726_b200 as P
-    from paper_2603_10726_b200.dist import (PeerExchange, ShardedIndex, TorchExchange, run_protocol,
-                                            run_protocol_device)
+    from paper_2603_10726_b200.dist import (PeerExchange, PeerUnavailable, ShardedIndex,
+                                            TorchExchange, run_protocol, run_protocol_device)
     from workloads import c2_shared_prompt
 
     per = 100_000 if args.config == "c2" else 10_000
@@ -525,14 +525,24 @@ def run_sharded(args, world, rank, local):
     shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
                          max_batch_tokens=s.n_tokens + 64, max_batch_requests=per, seed=SEED,
                          device=local)
-    # SOLID_DIST_EXCHANGE=p2p: the library's own exchange over peer memory;
-    # default: torch.distributed (NCCL, or gloo with host staging)
-    xport = os.environ.get("SOLID_DIST_EXCHANGE", "torch")
+    # The library's own exchange over peer memory: SOLID_DIST_EXCHANGE=p2p-dev
+    # (default: records stored into the peers' buffers by the pack kernels, device-resident
+    # counts) or p2p (host counts); =torch: torch.distributed (NCCL, or gloo with host staging).
+    # If some rank cannot map its peers (no CUDA IPC), every rank falls back to torch.
+    xport = os.environ.get("SOLID_DIST_EXCHANGE", "p2p-dev")
+    ex = None
     if xport in ("p2p", "p2p-dev"):
-        ex = PeerExchange(shard, device_counts=xport == "p2p-dev")
-        xname = "p2p (CUDA IPC peer stores + mailbox flags)" + (
-            ", device-resident counts" if xport == "p2p-dev" else "")
-    else:
+        try:
+            ex = PeerExchange(shard, device_counts=xport == "p2p-dev")
+            xname = "p2p (CUDA IPC peer stores + mailbox flags)" + (
+                ", device-resident counts" if xport == "p2p-dev" else "")
+        except PeerUnavailable as e:
+            print(f"[bench] {e}; falling back to torch.distributed", file=sys.stderr)
+            shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
+                                 max_batch_tokens=s.n_tokens + 64, max_batch_requests=per,
+                                 seed=SEED, device=local)
+            xport = "torch"
+    if ex is None:
         staging = os.environ.get("SOLID_DIST_BACKEND", "nccl") != "nccl"
         ex = TorchExchange(shard, staging=staging)
         xname = "gloo, host-staged" if staging else "nccl all_to_all + batched p2p"

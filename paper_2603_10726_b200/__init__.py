@@ -216,8 +216,11 @@ class Index:
 
     def _check(self, rc: int):
         if rc != SOLID_OK:
-            msg = self.lib.solid_last_error(self.h)
-            raise SolidError(rc, msg.decode() if msg else "")
+            raise SolidError(rc, self.last_error())
+
+    def last_error(self) -> str:
+        msg = self.lib.solid_last_error(self.h)
+        return msg.decode() if msg else ""
 
     @staticmethod
     def _stream(stream):

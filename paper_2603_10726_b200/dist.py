@@ -161,6 +161,11 @@ def loopback_admit(shards: List[ShardedIndex], local_batches, seq_bases):
     return run_protocol(shards, args, exchange, lambda xs: max(xs))
 
 
+class PeerUnavailable(RuntimeError):
+    """Some rank could not map its peers' regions (no CUDA IPC / peer access): raised on every
+    rank alike, so callers can fall back to another transport together."""
+
+
 class PeerExchange:
     """One shard per process on one node, records moved by the library itself over peer memory
     (solid_dist_p2p_*: CUDA IPC-mapped receive buffers, NVLink / NVSwitch stores, mailbox flags;
@@ -181,11 +186,18 @@ class PeerExchange:
         lib.solid_dist_p2p_exchange.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
                                                 ctypes.c_void_p, ctypes.c_void_p]
         mine = ctypes.create_string_buffer(64)
-        shard.index._check(lib.solid_dist_p2p_export(h, mine))
+        ok = lib.solid_dist_p2p_export(h, mine) == SOLID_OK
         allh = [None] * shard.world
-        dist.all_gather_object(allh, bytes(mine.raw), group=self.group)
-        table = ctypes.create_string_buffer(b"".join(allh), 64 * shard.world)
-        shard.index._check(lib.solid_dist_p2p_connect(h, table))
+        dist.all_gather_object(allh, bytes(mine.raw) if ok else b"", group=self.group)
+        ok = all(len(x) == 64 for x in allh)
+        if ok:
+            table = ctypes.create_string_buffer(b"".join(allh), 64 * shard.world)
+            ok = lib.solid_dist_p2p_connect(h, table) == SOLID_OK
+        votes = [None] * shard.world
+        dist.all_gather_object(votes, ok, group=self.group)
+        if not all(votes):
+            raise PeerUnavailable("peer-memory exchange unavailable on some rank: "
+                                  + shard.index.last_error())
         lib.solid_dist_p2p_device_counts.restype = ctypes.c_int
         lib.solid_dist_p2p_device_counts.argtypes = [ctypes.c_void_p, ctypes.c_uint32]
         lib.solid_dist_p2p_exchange_dev.restype = ctypes.c_int
