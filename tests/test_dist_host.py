@@ -124,3 +124,81 @@ def test_overflow_on_one_shard_rolls_back_everywhere():
     for rank, status, code, log in out:
         assert status == "err" and code == SOLID_ERR_CAPACITY
         assert log[-2:] == ["commit1", "commit2"]
+
+
+class FakeDevShard(FakeShard):
+    """Device-counts mode stand-in: the protocol passes no counts; the round's changed flag
+    travels with the next synchronised exchange (run_protocol_device)."""
+
+    def owner_ingest(self, phase, rc):
+        assert rc is None
+        self.log.append(f"ingest{phase}")
+
+    def round(self, t, rc):
+        assert rc is None
+        self.log.append(f"round{t}")
+        self.changed = int(t == 1 or (self.rank == 1 and t < self.converge_at))
+        return None, 0
+
+    def begin(self, *a):
+        self.log.append("begin")
+
+
+def _dev_worker(rank, world, port, overflow_rank, q):
+    from paper_2603_10726_b200.dist import run_protocol_device
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sh = FakeDevShard(world, rank, overflow=(rank == overflow_rank))
+
+        def exchange_dev(sync):
+            sh.log.append("x!" if sync else "x")
+            if not sync:
+                return 0
+            v = torch.tensor([sh.changed], dtype=torch.int64)     # the mailbox flags' max
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+            return int(v.item())
+
+        def allreduce_max(xs):
+            v = torch.tensor([max(xs)], dtype=torch.int64)
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+            return int(v.item())
+
+        try:
+            res, t = run_protocol_device(sh, (), exchange_dev, allreduce_max)
+            q.put((rank, "ok", t, sh.log))
+        except SolidError as e:
+            q.put((rank, "err", e.status, sh.log))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn_dev(overflow_rank):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dev_worker, args=(r, 2, port, overflow_rank, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(out)
+
+
+def test_device_counts_protocol_world2_gloo():
+    """run_protocol_device: REG and PULL exchanges asynchronous, one synchronised INT exchange
+    per round carrying the changed flag, same stop round as the host-counts protocol."""
+    for rank, status, t, log in _spawn_dev(overflow_rank=-1):
+        assert status == "ok" and t == 3
+        assert log == ["begin", "x", "ingest0", "x", "round1", "x!", "ingest1", "x", "round2",
+                       "x!", "ingest2", "x", "round3", "x!", "ingest3", "commit1"]
+
+
+def test_device_counts_overflow_rolls_back_everywhere():
+    for rank, status, code, log in _spawn_dev(overflow_rank=0):
+        assert status == "err" and code == SOLID_ERR_CAPACITY
+        assert log[-2:] == ["commit1", "commit2"]
