@@ -131,6 +131,7 @@ struct KParams {
   unsigned long long* int_flg;     // per local id: this round's earliest local flagger
   uint32_t* mown;                  // per local id: owner user of the mirrored first inserter
   uint32_t* long_q;                // K_A: requests longer than kLongBlocks (CTA path)
+  uint32_t* pool_cnt;              // block_table: k_commit counts each request's new entries
   // LRU eviction mode (solid_evict.inc): keys of the batch whose LRU record lies
   // in the eviction window get a window index w (their index snapshot is then visible only up
   // to their eviction time win_ev[w]); winfo[id] = epoch << 32 | w publishes an id's creation
@@ -1066,6 +1067,7 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
       if (itag == tag) {
         ++c_new;
         Cold* c = kp.cold + id;
+        if (mode == 1 && kp.pool_cnt) atomicAdd(&kp.pool_cnt[(uint32_t)pw[q].x - 1u], 1u);
         if (mode == 1) {
           const ulonglong2 val =
               make_ulonglong2(key[q], (unsigned long long)who[q] | ((unsigned long long)sharer[q] << 32));
@@ -1297,6 +1299,7 @@ struct solid_ctx {
   // LRU eviction mode (solid_evict.inc)
   struct Evict* ev_state = nullptr;
   struct Pool* pool = nullptr;     // block_table: physical blocks + block tables (solid_pool.inc)
+  uint32_t* pool_cnt = nullptr;    // its per-request new-entry counts (filled by k_commit)
   uint32_t* long_q = nullptr;      // K_A long-request queue (max_batch_requests entries)
 };
 
@@ -1653,6 +1656,7 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   // resident warps (148 SMs x 32): with more, warp-per-request already fills the machine and
   // the per-step CTA barriers cost more than they parallelise (C3: 1.64 vs 1.34 ms)
   kp.long_q = b->n_requests <= kLongMaxBatch ? ctx->long_q : nullptr;
+  kp.pool_cnt = ctx->pool_cnt;
   kp.seg_cnt = ctx->seg_cnt;
   kp.seg_cap = ctx->seg_cap;
   kp.st = ctx->st;
@@ -1701,6 +1705,7 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
 static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mode) {
   const uint64_t n = ctx->kp.n;
   if (n) {
+    if (ctx->kp.pool_cnt) CK(cudaMemsetAsync(ctx->kp.pool_cnt, 0, n * 4, s));
     launch_commit(ctx, 1, s);      // optimistic commit + count; exact rollback on overflow
     CK(cudaGetLastError());
     // asynchronous: k_stats' last CTA also takes the capacity decision on the device
