@@ -109,19 +109,49 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(stream, sample_requests: int):
-    """The oracle as it stands (sequential, one thread) on the first `sample_requests` requests."""
+    """The oracle as it stands (sequential, one thread) on the first `sample_requests` requests.
+    Returns (baseline object, oracle results, oracle index dump) — the last two let the caller
+    check the timed GPU step against the oracle on the same stream (parity of what is timed)."""
     from oracle import Oracle
     s = stream.slice(0, min(sample_requests, stream.n_requests))
     o = Oracle(16, SEED, 2)
     o.reserve(s.n_blocks() // 8 + 1024)
     t0 = time.perf_counter()
-    o.process(s)
+    res = o.process(s)
     dt = time.perf_counter() - t0
-    return {"value": s.n_requests / dt, "unit": "requests/s", "cores": 1, "kind": "oracle",
-            "blocks_per_s": s.n_blocks() / dt, "seconds": dt,
+    info = {"value": s.n_requests / dt, "unit": "requests/s", "cores": 1, "kind": "oracle",
+            "blocks_per_s": s.n_blocks() / dt, "seconds": dt, "host_cores": os.cpu_count(),
+            "cpu_model": _cpu_model(),
             "sample": f"first {s.n_requests} requests ({s.n_blocks()} blocks) of the same stream, "
                       f"sequential C++ oracle, 1 thread (host has {os.cpu_count()} cores)"}
+    return info, res, o.dump()
+
+
+def parity_of_timed_step(res, dump, exp, exp_dump):
+    """Element-by-element comparison of the last timed step's results and the index it left with
+    the oracle's on the same stream (every result field; key, owner, sharer of every entry)."""
+    fields = list(exp.dtype.names)
+    bad = {f: int((res[f].astype(np.int64) != exp[f].astype(np.int64)).sum()) for f in fields}
+    same_len = len(dump) == len(exp_dump)
+    bad_idx = {f: (int((dump[f] != exp_dump[f]).sum()) if same_len else None)
+               for f in ("key", "owner", "sharer")}
+    ok = same_len and not any(bad.values()) and not any(bad_idx.values())
+    return {"status": "exact" if ok else "MISMATCH", "requests": int(len(exp)),
+            "entries": int(len(exp_dump)), "result_fields": fields, "mismatches": bad,
+            "index_mismatches": bad_idx, "index_entries_gpu": int(len(dump)),
+            "what": "last timed step's solid_result[] and the index it committed vs the oracle "
+                    "on the same 100 000-request stream"}
 
 
 def measure_activator(dev, args):
@@ -716,7 +746,8 @@ def main():
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    phase = {"hash": [], "resolve": [], "commit": [], "hash_kernel": [], "round1": []}
+    phase = {"hash": [], "resolve": [], "commit": [], "hash_kernel": [], "round1": [],
+             "shared_keys": []}
     rounds, launches = [], []
     stats = None
     with ClockSampler(local) as clk:
@@ -728,7 +759,7 @@ def main():
             st = idx.stats()
             for key, f in [("hash", "ms_hash"), ("resolve", "ms_resolve"),
                            ("commit", "ms_commit"), ("hash_kernel", "ms_hash_kernel"),
-                           ("round1", "ms_round_first")]:
+                           ("round1", "ms_round_first"), ("shared_keys", "last_shared_keys")]:
                 phase[key].append(st[f])
             rounds.append(st["last_rounds"])
             launches.append(st["last_kernel_launches"])
@@ -758,8 +789,10 @@ def main():
     reqs_all = N * world
     value = reqs_all * args.steps / (tot_ms / 1000.0)
 
-    # correctness spot-check of the timed configuration (full check lives in tests/)
+    # the last timed step's results and index, checked against the oracle below (cpu_baseline
+    # runs the oracle on the same stream)
     res = P.as_numpy(out)
+    timed_dump = idx.dump()
 
     # roofline.  The kernel that moves the algorithmic bytes is k_hash_register (every token is
     # read there); the resolver rounds (k_eval) take the larger share of the step but carry no
@@ -767,7 +800,11 @@ def main():
     peak, peak_src = _peaks()
     alg_bytes = stats["algorithmic_bytes"]
     hash_ms = statistics.median(phase["hash_kernel"])
-    hash_bytes = 64 * nblk + 12 * N + 4 * nblk     # tokens + offsets/users + id per block
+    # SURVEY §8(d) bytes of K_A per launch: the tokens of every full block (64 B), offsets + user
+    # per request (12 B), and one 16-byte index slot per distinct key it probes (the snapshot of
+    # every Shared key of the batch); the 4 B/block id scratch is implementation, not counted
+    probes = statistics.median(phase["shared_keys"])
+    hash_bytes = 64 * nblk + 12 * N + 16 * probes
     step_ms = tot_ms / args.steps
     roof_step = alg_bytes / (step_ms / 1e3) / 1e9
     traffic, l2hit, res_inst = None, None, None
@@ -780,11 +817,15 @@ def main():
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": "k_hash_register (hash + scan + probe/register)",
+                "whole_step_frac": roof_step / peak,
                 "achieved": hash_bytes / (hash_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": hash_bytes / (hash_ms / 1e3) / 1e9 / peak, "traffic": traffic,
                 "traffic_source": "profiles/latest_ncu.json (ncu dram__bytes_read+write, same cmd)",
                 "l2_hit_pct": l2hit,
                 "algorithmic_bytes_per_launch": hash_bytes, "launch_ms": hash_ms,
+                "bytes_formula": "64 B x full blocks + 12 B x requests + 16 B x distinct keys "
+                                 "probed in the index (SURVEY 8(d))",
+                "snapshot_probes": probes,
                 "share_of_step": hash_ms / step_ms, "peak_source": peak_src,
                 "whole_step": {"achieved": roof_step, "frac": roof_step / peak,
                                "algorithmic_bytes": alg_bytes,
@@ -877,9 +918,13 @@ def main():
     if rank == 0 and world == 1 and not args.profile and not args.no_policy_eval:
         peval = measure_policy_eval(dev, args)
 
-    cpu = None
+    cpu, parity = None, {"status": "not checked (--no-cpu)"}
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        cpu = cpu_baseline(stream_np, args.cpu_sample)
+        cpu, exp_res, exp_dump = cpu_baseline(stream_np, args.cpu_sample)
+        if len(exp_res) == N:
+            parity = parity_of_timed_step(res, timed_dump, exp_res, exp_dump)
+        else:
+            parity = {"status": f"not checked (oracle sample {len(exp_res)} < {N} requests)"}
 
     if world > 1:
         dist.barrier()
@@ -901,6 +946,7 @@ def main():
             "roofline": roofline,
             "resolver_roofline": resolver_roofline,
             "cpu_baseline": cpu,
+            "parity": parity,
             "activator": activator,
             "lru_eviction": lru,
             "hash_components_2": hash2,

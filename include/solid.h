@@ -39,7 +39,9 @@ typedef enum {
   SOLID_ERR_CAPACITY = 2,  /* index or scratch would overflow; nothing was mutated             */
   SOLID_ERR_STATE = 3,     /* call order violated, or context poisoned by an earlier failure  */
   SOLID_ERR_CUDA = 4,      /* CUDA runtime error (context poisoned)                           */
-  SOLID_ERR_NCCL = 5,      /* reserved for the sharded multi-GPU index          */
+  SOLID_ERR_NCCL = 5,      /* sharded index: the record transport failed (a peer did not post
+                              its exchange within 60 s, or a collective failed); nothing of
+                              the batch was committed on this shard                        */
   SOLID_ERR_OOM = 6        /* device allocation failed in solid_init                          */
 } solid_status;
 
@@ -149,7 +151,8 @@ typedef struct {
   uint32_t max_evict_iters;      /* max resolver / eviction-time iterations of any batch     */
   uint32_t rebuilds;             /* index rebuilds (tombstone clean-up), cumulative          */
   uint32_t compactions;          /* LRU log compactions, cumulative                          */
-  uint32_t reserved2;
+  uint32_t last_shared_keys;     /* distinct keys registered (and probed in the index) by the
+                                    hash kernel K_A, last batch: its snapshot probes (§8(d))  */
 } solid_stats_t;
 
 uint32_t solid_abi_version(void);
@@ -166,7 +169,9 @@ solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* batch, solid_
                                 void* stream);
 
 /* Commit the staged admissions of the last lookup: 128-bit CAS claims {key, owner, sharer}
- * for new entries and sharer writes on flagged existing entries.  Checks capacity first.
+ * for new entries and sharer writes on flagged existing entries.  Checks capacity first: the
+ * batch's new entries are counted on the device (k_stats) before any claim, and a batch with
+ * live + new > capacity_blocks claims nothing and fails with SOLID_ERR_CAPACITY.
  * Evict mode: also removes the batch's LRU victims (tombstones) and appends the LRU records of
  * every entry the batch touched; a batch that would have to evict an entry it touched itself
  * (it inserts more entries than the index holds untouched ones) fails with SOLID_ERR_CAPACITY
@@ -176,8 +181,8 @@ solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* batch, solid_
 solid_status solid_insert_batch(solid_ctx* ctx, void* stream);
 
 /* Asynchronous admission (lookup + insert with no host synchronisation), for a pipelined caller.
- * The capacity check (R9) and the exact rollback of an over-capacity batch run on the device, so
- * every batch is still all-or-nothing and batches apply in submission order; a failed batch
+ * The capacity check (R9) runs on the device before any claim (an over-capacity batch claims
+ * nothing), so every batch is still all-or-nothing and batches apply in submission order; a failed batch
  * leaves the index exactly as before it, and later batches see that state.  Up to
  * SOLID_MAX_INFLIGHT batches may be outstanding; each must be collected, oldest first, by
  * solid_batch_status, which waits for it and returns ITS status (SOLID_OK, SOLID_ERR_INVALID,
@@ -217,6 +222,16 @@ solid_status solid_stats(solid_ctx* ctx, solid_stats_t* out);
 /* Test hook: set the batch-scratch epoch (tags restart, with a scratch re-initialisation, after
  * ~2^20 batches; tests jump close to the limit).  SOLID_ERR_STATE with a batch in flight. */
 solid_status solid_debug_set_epoch(solid_ctx* ctx, uint32_t epoch);
+
+/* Test hook: the resolver's round limit (2..4093, default 4093).  Requests
+ * before round t are final after round t, so a batch of <= limit - 1 requests always converges.
+ * A batch that does not converge is committed in consecutive parts (halves, recursively; the
+ * results equal one admission by R1) by solid_insert_batch / solid_admit_host; through
+ * solid_admit_batch it fails with SOLID_ERR_STATE and commits nothing (later batches in flight
+ * see the index without it), and the caller resubmits it in parts.  Block tables / block keys
+ * are not produced for a batch committed in parts (SOLID_ERR_STATE), and a block_table context
+ * does not split (SOLID_ERR_STATE).  SOLID_ERR_STATE with a batch in flight. */
+solid_status solid_debug_set_max_rounds(solid_ctx* ctx, uint32_t rounds);
 
 /* Block table of the last admitted batch (paged-KV integration; call after
  * solid_insert_batch, or after solid_batch_status collected the last solid_admit_batch, and
@@ -314,6 +329,9 @@ const char* solid_last_error(const solid_ctx* ctx);
  *     changed = max over ranks of solid_dist_round's flag; stop when t >= 2 and !changed
  *                (APC / USER_ISOLATION: stop after t = 1)
  *   solid_dist_commit(mode 1); if any rank reports overflow: solid_dist_commit(mode 2)
+ *     (mode 1 counts the shard's new entries first and claims nothing when they would exceed
+ *     capacity_blocks, returning SOLID_ERR_CAPACITY; mode 2 then rolls back the shards that
+ *     did commit and is a no-op on the others)
  *
  * Records are 24 bytes.  Send region for peer d starts at record d * cap_records of the send
  * buffer; receive region for peer s at record s * cap_records of the receive buffer.  Counts

@@ -36,7 +36,7 @@ HIT, MISS, EXCLUDED = 0, 1, 2
 class ActivatorConfig:
     theta: float = 0.5          # P:523 threshold θ in [0, 1]
     window_len: int = 256       # samples kept per class
-    min_samples: int = 2        # fewer in either class -> fail-safe active
+    min_samples: int = 16       # fewer in either class -> fail-safe active (default)
     hit_hi: float = 0.8         # reuse fraction >= hit_hi -> Hit
     hit_lo: float = 0.2         # reuse fraction <= hit_lo -> Miss
     grid: int = 512             # trapezoid points

@@ -30,7 +30,7 @@ ENTRY_EX_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4"),
 # C ABI entry points declared in include/solid.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
                "solid_insert_batch", "solid_admit_host", "solid_admit_host_u16", "solid_stats", "solid_dump", "solid_dump_ex",
-               "solid_admit_batch", "solid_batch_status", "solid_block_keys", "solid_debug_set_epoch",
+               "solid_admit_batch", "solid_batch_status", "solid_block_keys", "solid_debug_set_epoch", "solid_debug_set_max_rounds",
                "solid_block_table", "solid_dump_phys",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
@@ -82,7 +82,7 @@ class _Stats(ctypes.Structure):
                 ("last_evict_iters", ctypes.c_uint32), ("last_window_keys", ctypes.c_uint32),
                 ("window_evicted", ctypes.c_uint64), ("max_evict_iters", ctypes.c_uint32),
                 ("rebuilds", ctypes.c_uint32), ("compactions", ctypes.c_uint32),
-                ("reserved2", ctypes.c_uint32)]
+                ("last_shared_keys", ctypes.c_uint32)]
 
 
 class _ActConfig(ctypes.Structure):
@@ -129,6 +129,8 @@ def load_library(path: str = LIB_PATH):
     lib.solid_dump.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
     lib.solid_debug_set_epoch.restype = st
     lib.solid_debug_set_epoch.argtypes = [vp, ctypes.c_uint32]
+    lib.solid_debug_set_max_rounds.restype = st
+    lib.solid_debug_set_max_rounds.argtypes = [vp, ctypes.c_uint32]
     lib.solid_block_keys.restype = st
     lib.solid_block_keys.argtypes = [vp, vp, vp]
     lib.solid_dump_ex.restype = st
@@ -403,6 +405,11 @@ class Index:
         """Test hook (solid_debug_set_epoch): jump the scratch epoch towards its restart."""
         self._check(self.lib.solid_debug_set_epoch(self.h, epoch))
 
+    def debug_set_max_rounds(self, rounds: int):
+        """Test hook (solid_debug_set_max_rounds): the resolver's round limit; a synchronous
+        admission that does not converge within it is committed in parts."""
+        self._check(self.lib.solid_debug_set_max_rounds(self.h, rounds))
+
     def checkpoint(self):
         self._check(self.lib.solid_checkpoint(self.h))
 
@@ -435,7 +442,7 @@ class Activator:
     """The Activator (solid_activator_*): per-request enforce bits from the KDE overlap of the
     hit / miss per-token-TTFT windows (estimator SPEC S:245-268)."""
 
-    def __init__(self, theta: float = 0.5, window_len: int = 256, min_samples: int = 2,
+    def __init__(self, theta: float = 0.5, window_len: int = 256, min_samples: int = 16,
                  hit_hi: float = 0.8, hit_lo: float = 0.2, grid: int = 512,
                  max_samples: int = 1 << 20, max_queries: int = 1 << 20, device: int = 0):
         self.lib = load_library()

@@ -50,7 +50,8 @@ constexpr uint32_t kMaxRounds = 4093;
 constexpr uint32_t kMaxEpoch = (0xFFFFFFFFu / 4096u) - 1;
 
 enum : uint32_t {
-  ERR_OFFSETS = 1, ERR_TOKEN = 2, ERR_USER = 4, ERR_BLOCKS = 8, ERR_SCRATCH = 16, ERR_SLOTCAP = 32
+  ERR_OFFSETS = 1, ERR_TOKEN = 2, ERR_USER = 4, ERR_BLOCKS = 8, ERR_SCRATCH = 16, ERR_SLOTCAP = 32,
+  ERR_TIMEOUT = 64   // sharded: a peer never posted its exchange (peer-memory transport)
 };
 
 struct __align__(32) Hot {            // staged state of one key, ping-pong by round parity P:
@@ -75,6 +76,7 @@ struct DevStatus {
   uint32_t long_cnt;                     // K_A: requests handed to the CTA-per-request path
   uint32_t long_head;                    // its work counter
   unsigned long long live_after;         // asynchronous admission: live entries after this batch
+  unsigned long long ids_after_hash;     // distinct keys registered by K_A (its snapshot probes)
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t seg[kNSeg];                   // id counts per segment (gathered by k_stats)
@@ -106,6 +108,7 @@ struct KParams {
   const uint32_t* users;
   const uint8_t* enforce;
   uint64_t n;
+  uint64_t j_lo;                   // resolver / stats: requests [j_lo, n) (a split batch's part)
   uint32_t max_blocks;
   uint32_t epoch;
   unsigned long long salt;         // per-epoch key salt of the batch key table
@@ -500,10 +503,10 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
 }
 
 template <int POLICY, int NC>
-__global__ void __launch_bounds__(256, 4) k_hash_register(KParams kp) {
+__global__ void __launch_bounds__(256, 4) k_hash_register(KParams kp, uint64_t j_lo, uint64_t j_hi) {
   const int lane = threadIdx.x & 31;
-  const uint64_t j = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (j >= kp.n) return;
+  const uint64_t j = j_lo + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (j >= j_hi) return;
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
   const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
   const uint32_t u = kp.users[j];
@@ -631,30 +634,36 @@ __global__ void __launch_bounds__(256, 4) k_hash_register_long(KParams kp) {
   }
 }
 
-// K_A on stream s (single GPU and sharded paths).
+// K_A on stream s (single GPU and sharded paths), for requests [lo, hi) of the batch (host
+// admission hashes each sub-range as soon as its tokens have arrived).
 template <int NC>
-static void launch_hash_nc(const KParams& kp, unsigned grid, cudaStream_t s) {
+static void launch_hash_nc(const KParams& kp, unsigned grid, uint64_t lo, uint64_t hi,
+                           cudaStream_t s) {
   const unsigned lg = 148 * 4;   // persistent CTAs for the long requests (none: they exit at once)
   switch (kp.policy) {
     case SOLID_POLICY_APC:
-      k_hash_register<SOLID_POLICY_APC, NC><<<grid, 256, 0, s>>>(kp);
+      k_hash_register<SOLID_POLICY_APC, NC><<<grid, 256, 0, s>>>(kp, lo, hi);
       if (kp.long_q) k_hash_register_long<SOLID_POLICY_APC, NC><<<lg, 256, 0, s>>>(kp);
       break;
     case SOLID_POLICY_USER_ISOLATION:
-      k_hash_register<SOLID_POLICY_USER_ISOLATION, NC><<<grid, 256, 0, s>>>(kp);
+      k_hash_register<SOLID_POLICY_USER_ISOLATION, NC><<<grid, 256, 0, s>>>(kp, lo, hi);
       if (kp.long_q) k_hash_register_long<SOLID_POLICY_USER_ISOLATION, NC><<<lg, 256, 0, s>>>(kp);
       break;
     default:
-      k_hash_register<SOLID_POLICY_SOLIDARITY, NC><<<grid, 256, 0, s>>>(kp);
+      k_hash_register<SOLID_POLICY_SOLIDARITY, NC><<<grid, 256, 0, s>>>(kp, lo, hi);
       if (kp.long_q) k_hash_register_long<SOLID_POLICY_SOLIDARITY, NC><<<lg, 256, 0, s>>>(kp);
       break;
   }
 }
-static cudaError_t launch_hash(const KParams& kp, cudaStream_t s) {
-  const unsigned grid = (unsigned)((kp.n * 32 + 255) / 256);
-  if (kp.nc == 2) launch_hash_nc<2>(kp, grid, s);
-  else launch_hash_nc<1>(kp, grid, s);
+static cudaError_t launch_hash(const KParams& kp, cudaStream_t s, uint64_t lo, uint64_t hi) {
+  if (hi <= lo) return cudaSuccess;
+  const unsigned grid = (unsigned)(((hi - lo) * 32 + 255) / 256);
+  if (kp.nc == 2) launch_hash_nc<2>(kp, grid, lo, hi, s);
+  else launch_hash_nc<1>(kp, grid, lo, hi, s);
   return cudaGetLastError();
+}
+static cudaError_t launch_hash(const KParams& kp, cudaStream_t s) {
+  return launch_hash(kp, s, 0, kp.n);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -977,12 +986,20 @@ __global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) 
   const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   if (grid.thread_rank() == 0) kp.st->round_ns[0] = globaltimer_ns();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {     // K_A's distinct keys (its index probes)
+    unsigned long long c = 0;
+#pragma unroll
+    for (int q = 0; q < kNSeg / 32; ++q) c += min(kp.seg_cnt[lane + 32 * q].v, kp.seg_cap);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) kp.st->ids_after_hash = c;
+  }
   __shared__ uint32_t s_changed;
   for (uint32_t t = 1; t <= t_max; ++t) {
     if (threadIdx.x == 0) s_changed = 0;
     __syncthreads();
     bool any = false;
-    for (uint64_t j = w0; j < kp.n; j += nw) any |= eval_request<POLICY, false>(kp, t, j, lane);
+    for (uint64_t j = kp.j_lo + w0; j < kp.n; j += nw)
+      any |= eval_request<POLICY, false>(kp, t, j, lane);
     // one store per CTA (100k same-address stores would serialise on one L2 slice)
     if (lane == 0 && any) s_changed = 1;
     __syncthreads();
@@ -1015,24 +1032,26 @@ __global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) 
 // key carrying the final round's tag was inserted by the request in its low 32 bits (the
 // earliest one, "set exactly once"): it claims an index slot with one 128-bit CAS
 // {key, owner, sharer}.  A snapshot entry whose flag carries the final tag gets its sharer
-// written (a6).  mode 1 commits (optimistically) and counts; mode 2 rolls the batch back exactly:
-// every claimed slot was EMPTY before, so emptying it again restores the previous probe chains.
+// written (a6).  k_stats ran first and counted the batch's new entries: on a capacity overflow
+// (R9) it set st->overflow and nothing is claimed — so live + new <= capacity <= tcap / 2 holds
+// for every claim and the linear probe always meets an EMPTY slot.  mode 2 rolls a committed
+// batch back exactly (every claimed slot was EMPTY before: emptying it restores the chains).
 // ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t final_round(const KParams& kp) {
+  return kp.st->conv == 0 ? 0 : (POLICY_IS_SOLIDARITY(kp) ? kp.st->conv : 0);
+}
+
 __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
   constexpr int U = 4;                 // ids per thread, staged so all loads are in flight at once
-  // the converged round is read on the device (lookup never waits for the host); an invalid or
-  // unconverged batch commits nothing
+  // the converged round is read on the device (lookup never waits for the host); an invalid,
+  // unconverged or over-capacity batch commits nothing
   if (kp.st->err || (kp.n && kp.st->conv == 0)) return;
-  if (mode == 3) {                       // device-decided rollback (asynchronous admission)
-    if (!kp.st->overflow) return;
-    mode = 2;
-  }
-  const uint32_t tf = kp.st->conv == 0 ? 0 : (POLICY_IS_SOLIDARITY(kp) ? kp.st->conv : 0);
+  if (mode == 1 && kp.st->overflow) return;
+  const uint32_t tf = final_round(kp);
   const uint32_t seg = blockIdx.y;
   const uint32_t cnt = min(kp.seg_cnt[seg].v, kp.seg_cap);
   const int W = (int)(tf & 1);
   const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
-  uint32_t c_new = 0, c_flag = 0;
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t x0 = blockIdx.x * blockDim.x + threadIdx.x; x0 < cnt; x0 += U * stride) {
     ulonglong2 pw[U];
@@ -1065,14 +1084,13 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
       const uint32_t id = seg * kp.seg_cap + x0 + q * stride + 1;
       const uint32_t itag = (uint32_t)(pw[q].x >> 32);
       if (itag == tag) {
-        ++c_new;
         Cold* c = kp.cold + id;
         if (mode == 1 && kp.pool_cnt) atomicAdd(&kp.pool_cnt[(uint32_t)pw[q].x - 1u], 1u);
         if (mode == 1) {
           const ulonglong2 val =
               make_ulonglong2(key[q], (unsigned long long)who[q] | ((unsigned long long)sharer[q] << 32));
           uint64_t p = key[q] & kp.tmask;
-          for (;;) {
+          for (;;) {   // terminates: at most capacity <= tcap / 2 slots are live (k_stats)
             const ulonglong2 old = atomic_cas128(&kp.tab[p], make_ulonglong2(0ull, 0ull), val);
             if (old.x == 0 || old.x == key[q]) break;
             p = (p + 1) & kp.tmask;
@@ -1082,64 +1100,25 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
           kp.tab[c->psl] = make_ulonglong2(0ull, 0ull);
         }
       } else if (itag == tagS && (uint32_t)(pw[q].y >> 32) == tag) {
-        ++c_flag;
         uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
         if (mode == 1) atomicCAS(sharer_word, kNone, who[q]);
         else atomicCAS(sharer_word, who[q], kNone);
       }
     }
   }
-  // one atomic per CTA (per-warp atomics on one counter serialise on a single L2 slice)
-  __shared__ uint32_t s_new, s_flag;
-  if (threadIdx.x == 0) s_new = s_flag = 0;
-  __syncthreads();
-  for (int o = 16; o; o >>= 1) {
-    c_new += __shfl_xor_sync(0xffffffffu, c_new, o);
-    c_flag += __shfl_xor_sync(0xffffffffu, c_flag, o);
-  }
-  if ((threadIdx.x & 31) == 0 && (c_new | c_flag)) {
-    atomicAdd(&s_new, c_new);
-    atomicAdd(&s_flag, c_flag);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && mode == 1 && (s_new | s_flag)) {
-    atomicAdd(&kp.st->new_entries, (unsigned long long)s_new);
-    atomicAdd(&kp.st->new_flags, (unsigned long long)s_flag);
-  }
 }
 
-// Exact rollback of a committed batch by one CTA (the asynchronous path's device-decided
-// capacity overflow, R9): every slot the batch claimed was EMPTY before — empty it again — and
-// every sharer it wrote was NONE.  Rare (an error path), so a single CTA is enough.
-__device__ void rollback_all(const KParams& kp) {
-  const uint32_t tf = kp.st->conv == 0 ? 0 : (POLICY_IS_SOLIDARITY(kp) ? kp.st->conv : 0);
-  const int W = (int)(tf & 1);
-  const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
-  for (uint32_t seg = 0; seg < (uint32_t)kNSeg; ++seg) {
-    const uint32_t cnt = min(kp.seg_cnt[seg].v, kp.seg_cap);
-    for (uint32_t x = threadIdx.x; x < cnt; x += blockDim.x) {
-      const uint32_t id = seg * kp.seg_cap + x + 1;
-      const ulonglong2 pw = ldw128(&kp.hot[id].v[2 * W]);
-      const uint32_t itag = (uint32_t)(pw.x >> 32);
-      if (itag == tag) {
-        kp.tab[kp.cold[id].psl] = make_ulonglong2(0ull, 0ull);
-      } else if (itag == tagS && (uint32_t)(pw.y >> 32) == tag) {
-        uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
-        atomicCAS(sharer_word, kp.users[(uint32_t)pw.y - 1u], kNone);
-      }
-    }
-  }
-}
-
-// Per-batch sums over the results (block-weighted hit rate).
-// With `live` set (asynchronous admission) the last CTA also takes the capacity decision (R9):
-// the live count stays resident on the device and an overflow is flagged for the rollback.
+// K_D, before the commit: per-batch sums over the results (block-weighted hit rate) and
+// the batch's new entries / new flags counted from the converged staged state (one 16-byte read
+// per key id).  With `live` set, the last CTA takes the capacity decision (R9): live + new >
+// capacity -> st->overflow (k_commit then claims nothing, the batch fails with
+// SOLID_ERR_CAPACITY), else live += new.  The live count stays resident on the device.
 __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t n,
                                                DevStatus* st, unsigned long long* live,
                                                unsigned long long cap, const SegCounter* seg,
                                                KParams kp) {
   if (blockIdx.x == 0 && threadIdx.x < kNSeg) st->seg[threadIdx.x] = seg[threadIdx.x].v;
-  unsigned long long a[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const solid_result r = out[j];
@@ -1150,37 +1129,48 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
     a[4] += (r.bits >> 3) & 1;
     a[5] += 1;
   }
-  __shared__ unsigned long long s_a[6];
-  if (threadIdx.x < 6) s_a[threadIdx.x] = 0;
+  const bool ok = live && !st->err && !(n && st->conv == 0);
+  if (ok) {                            // new entries (a[6]) and new sharer writes (a[7])
+    const uint32_t tf = final_round(kp);
+    const int W = (int)(tf & 1);
+    const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t sg = 0; sg < (uint32_t)kNSeg; ++sg) {
+      const uint32_t cnt = min(seg[sg].v, kp.seg_cap);
+      for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += stride) {
+        const ulonglong2 pw = ldw128(&kp.hot[sg * kp.seg_cap + x + 1].v[2 * W]);
+        const uint32_t itag = (uint32_t)(pw.x >> 32);
+        a[6] += itag == tag;
+        a[7] += itag == tagS && (uint32_t)(pw.y >> 32) == tag;
+      }
+    }
+  }
+  __shared__ unsigned long long s_a[8];
+  if (threadIdx.x < 8) s_a[threadIdx.x] = 0;
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < 6; ++q) {
+  for (int q = 0; q < 8; ++q) {
     for (int o = 16; o; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
     if ((threadIdx.x & 31) == 0 && a[q]) atomicAdd(&s_a[q], a[q]);
   }
   __syncthreads();
   if (threadIdx.x < 6 && s_a[threadIdx.x]) atomicAdd(&st->sums[threadIdx.x], s_a[threadIdx.x]);
+  if (threadIdx.x == 6 && s_a[6]) atomicAdd(&st->new_entries, s_a[6]);
+  if (threadIdx.x == 7 && s_a[7]) atomicAdd(&st->new_flags, s_a[7]);
   if (!live) return;
-  __shared__ bool s_last, s_ovf;
+  __shared__ bool s_last;
+  __threadfence();                     // this CTA's sums are visible before it is counted done
+  __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!s_last) return;
-  if (threadIdx.x == 0) {             // new_entries is final: k_commit completed before us
-    __threadfence();
-    s_ovf = false;
-    if (!st->err) {
-      const unsigned long long l = *live, add = st->new_entries;
-      if (l + add > cap) {
-        st->overflow = 1;
-        s_ovf = true;
-      } else {
-        *live = l + add;
-      }
-    }
-    st->live_after = *live;
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  if (ok) {
+    const unsigned long long l = *live, add = *(volatile unsigned long long*)&st->new_entries;
+    if (l + add > cap) st->overflow = 1;
+    else *live = l + add;
   }
-  __syncthreads();
-  if (s_ovf) rollback_all(kp);        // the batch leaves the index exactly as before it
+  st->live_after = *live;
 }
 
 // Compact the live index slots (dump): warp-aggregated append.
@@ -1270,13 +1260,14 @@ struct solid_ctx {
   KParams kp{};
   uint32_t tf = 0;
   uint32_t rounds = 0;
+  uint32_t max_rounds = kMaxRounds;      // resolver round limit (solid_debug_set_max_rounds)
+  bool split_last = false;               // the last batch was committed in parts (non-convergence)
   cudaStream_t stream = nullptr;
   // host-buffer admission staging
   uint32_t* h_tokens = nullptr;
   uint16_t* h_tokens16 = nullptr;
   cudaStream_t s_copy = nullptr;               // host admission: token copies of later chunks
   cudaEvent_t ev_chunk[kHostChunks + 1] = {};
-  uint64_t* h_offs_sub = nullptr;
   uint64_t* h_offsets = nullptr;
   uint32_t* h_users = nullptr;
   uint8_t* h_enforce = nullptr;
@@ -1354,6 +1345,7 @@ static solid_status pool_pre(solid_ctx* ctx, cudaStream_t s, uint32_t tf);
 static solid_status pool_commit(solid_ctx* ctx, cudaStream_t s, uint32_t tf, uint64_t new_entries,
                                 uint64_t evicted, uint64_t ebound);
 static solid_status pool_checkpoint(solid_ctx* ctx);
+static void pool_invalidate(solid_ctx* ctx);
 static solid_status pool_restore(solid_ctx* ctx);
 
 static void free_all(solid_ctx* c) {
@@ -1379,7 +1371,6 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->cs);
   cudaFree(c->h_tokens);
   cudaFree(c->h_tokens16);
-  cudaFree(c->h_offs_sub);
   for (auto& e : c->ev_chunk)
     if (e) cudaEventDestroy(e);
   if (c->s_copy) cudaStreamDestroy(c->s_copy);
@@ -1578,9 +1569,9 @@ static solid_status launch_resolve(solid_ctx* ctx, cudaStream_t s) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
     ctx->resolve_ctas = (uint64_t)per_sm * sms;
   }
-  const uint64_t need = (ctx->kp.n * 32 + 255) / 256;
+  const uint64_t need = ((ctx->kp.n - ctx->kp.j_lo) * 32 + 255) / 256;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ctx->resolve_ctas, need));
-  uint32_t tmax = kMaxRounds;
+  uint32_t tmax = ctx->max_rounds;
   void* args[] = {(void*)&ctx->kp, (void*)&tmax};
   CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, s));
   return SOLID_OK;
@@ -1590,8 +1581,12 @@ static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
   k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, mode);   // 4 staged ids per thread
 }
 
-static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result* out,
-                             void* stream) {
+// Validates the batch and prepares the kernel parameters of a lookup (no kernel launched yet).
+static solid_status admit_range(solid_ctx* ctx, uint64_t lo, uint64_t hi, cudaStream_t s);
+static solid_status lookup_resolve(solid_ctx* ctx, cudaStream_t s);
+
+static solid_status lookup_setup(solid_ctx* ctx, const solid_batch* b, solid_result* out,
+                                 void* stream) {
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "lookup_batch twice without insert_batch");
   if (ctx->dist) return fail(ctx, SOLID_ERR_STATE, "sharded context: use the solid_dist_* calls");
@@ -1635,6 +1630,8 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   kp.users = b->users;
   kp.enforce = b->enforce;
   kp.n = b->n_requests;
+  kp.j_lo = 0;
+  ctx->split_last = false;
   kp.policy = ctx->cfg.policy;
   kp.seq_base = 0;
   kp.dist = 0;
@@ -1662,17 +1659,18 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   kp.st = ctx->st;
   CK(cudaMemsetAsync(ctx->st, 0, kStHead, s));
   CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
-  if (ctx->ev_state) return evict_lookup(ctx, s);
-  CK(cudaEventRecord(ctx->ev[0], s));
-  const uint64_t n = b->n_requests;
+  // the block table describes the last COMMITTED batch; this lookup replaces the batch arrays it
+  // is built from, so it is unavailable until this batch commits
+  pool_invalidate(ctx);
   ctx->launches = 0;
-  if (n) {
-    CK(launch_hash(kp, s));
-    ctx->launches = 1;
-  }
+  return SOLID_OK;
+}
+
+// After K_A: the resolver; the lookup is then pending (solid_insert_batch commits it).
+static solid_status lookup_resolve(solid_ctx* ctx, cudaStream_t s) {
   CK(cudaEventRecord(ctx->ev[1], s));
   CK(cudaEventRecord(ctx->ev[4], s));
-  if (n) {
+  if (ctx->kp.n) {
     solid_status rc = launch_resolve(ctx, s);
     if (rc != SOLID_OK) return rc;
     ctx->launches += 1;
@@ -1681,6 +1679,20 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   CK(cudaEventRecord(ctx->ev[2], s));
   ctx->pending = true;
   return SOLID_OK;
+}
+
+static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result* out,
+                             void* stream) {
+  solid_status rc = lookup_setup(ctx, b, out, stream);
+  if (rc != SOLID_OK) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ctx->ev_state) return evict_lookup(ctx, s);
+  CK(cudaEventRecord(ctx->ev[0], s));
+  if (ctx->kp.n) {
+    CK(launch_hash(ctx->kp, s));
+    ctx->launches = 1;
+  }
+  return lookup_resolve(ctx, s);
 }
 
 static solid_status require_collected(solid_ctx* ctx, const char* what) {
@@ -1700,20 +1712,18 @@ extern "C" solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* b,
   return do_lookup(ctx, b, out, stream);
 }
 
-// Enqueue the commit of the pending lookup (+ stats and the status copies).  async_mode: the
-// capacity check and the exact rollback also run on the device (no host decision).
-static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s, bool async_mode) {
-  const uint64_t n = ctx->kp.n;
+// Enqueue the commit of the pending lookup (+ stats and the status copies).  The capacity check
+// runs on the device before any claim (k_stats), for the synchronous and asynchronous paths.
+static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s) {
+  const uint64_t n = ctx->kp.n - ctx->kp.j_lo;
   if (n) {
-    if (ctx->kp.pool_cnt) CK(cudaMemsetAsync(ctx->kp.pool_cnt, 0, n * 4, s));
-    launch_commit(ctx, 1, s);      // optimistic commit + count; exact rollback on overflow
-    CK(cudaGetLastError());
-    // asynchronous: k_stats' last CTA also takes the capacity decision on the device
-    // asynchronous: k_stats' last CTA also takes the capacity decision and, on overflow, rolls
-    // the batch back itself (no extra launch per batch)
+    if (ctx->kp.pool_cnt) CK(cudaMemsetAsync(ctx->kp.pool_cnt, 0, ctx->kp.n * 4, s));
+    // counts and the capacity decision first (device-resident live count), then the claims
     k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
-        ctx->kp.out, n, ctx->st, async_mode ? ctx->live_dev : nullptr, ctx->cfg.capacity_blocks,
+        ctx->kp.out + ctx->kp.j_lo, n, ctx->st, ctx->live_dev, ctx->cfg.capacity_blocks,
         ctx->seg_cnt, ctx->kp);
+    CK(cudaGetLastError());
+    launch_commit(ctx, 1, s);
     CK(cudaGetLastError());
     ctx->launches += 2;
   }
@@ -1745,17 +1755,11 @@ static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, boo
     return fail(ctx, SOLID_ERR_INVALID, m);
   }
   if (n && h.conv == 0)
-    return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within 4093 rounds");
+    return fail(ctx, SOLID_ERR_STATE, "resolver did not converge within the round limit "
+                                      "(nothing committed; resubmit the batch in parts)");
   const bool current = f.gen == ctx->gen;
-  if (async_mode) {
-    if (h.overflow)
-      return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9); rolled back");
-  } else if (n && ctx->live + h.new_entries > ctx->cfg.capacity_blocks) {
-    launch_commit(ctx, 2, s);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(s));
-    return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9)");
-  }
+  if (h.overflow)
+    return fail(ctx, SOLID_ERR_CAPACITY, "index capacity exceeded (no eviction, R9); nothing committed");
   if (ctx->pool && current && !async_mode) {   // physical blocks (solid_pool.inc)
     solid_status rc = pool_commit(ctx, s, ctx->cfg.policy == SOLID_POLICY_SOLIDARITY ? h.conv : 0u,
                                   h.new_entries, 0, 0);
@@ -1772,13 +1776,7 @@ static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, boo
     S.diverted += h.sums[3];
     S.truncated += h.sums[4];
     S.inserted += h.new_entries;
-    if (async_mode) {
-      if (n) ctx->live = h.live_after;
-    } else {
-      ctx->live += h.new_entries;
-      CK(cudaMemcpyAsync(ctx->live_dev, &ctx->live, sizeof(unsigned long long),
-                         cudaMemcpyHostToDevice, s));
-    }
+    if (n) ctx->live = h.live_after;
     S.live_entries = ctx->live;
   }
   S.last_rounds = ctx->rounds;
@@ -1790,6 +1788,7 @@ static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, boo
   for (int q = 0; q < kNSeg; ++q)
     distinct += std::min<uint32_t>(ctx->slots[i].st.seg[q], ctx->seg_cap);
   S.last_distinct_keys = (uint32_t)std::min<uint64_t>(distinct, 0xFFFFFFFFull);
+  S.last_shared_keys = (uint32_t)std::min<unsigned long long>(h.ids_after_hash, 0xFFFFFFFFull);
   S.last_kernel_launches = f.launches;
   S.last_requests = n;
   S.last_blocks = h.sums[0];
@@ -1813,11 +1812,48 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(ctx->dev));
   if (ctx->ev_state) return evict_insert(ctx, s);
-  solid_status rc = enqueue_commit(ctx, s, false);
+  solid_status rc = enqueue_commit(ctx, s);
   if (rc != SOLID_OK) return rc;
   CK(cudaStreamSynchronize(s));
   ctx->pending = false;
+  const DevStatus& h = ctx->slots[ctx->cur].st;
+  if (ctx->kp.n > ctx->kp.j_lo && h.conv == 0 && h.err == 0 && !ctx->pool) {
+    // the resolver hit its round limit: nothing was committed.  Requests
+    // before round t_max are final, so admitting the batch as consecutive parts (R1: results
+    // do not depend on the cut) always ends: a part of <= t_max - 1 requests converges.
+    const uint64_t lo = ctx->kp.j_lo, hi = ctx->kp.n;
+    if (hi - lo < 2) return fail(ctx, SOLID_ERR_STATE, "resolver did not converge");
+    const uint64_t mid = lo + (hi - lo) / 2;
+    rc = admit_range(ctx, lo, mid, s);
+    if (rc == SOLID_OK) rc = admit_range(ctx, mid, hi, s);
+    ctx->split_last = true;
+    return rc;
+  }
   return finish_batch(ctx, ctx->cur, s, false);
+}
+
+// Admit requests [lo, hi) of the pending batch's arrays as a batch of their own (a part of a
+// batch whose resolver did not converge; R1: admitting a stream in consecutive parts gives the
+// same results).  Synchronous; splits again if the part does not converge either.
+static solid_status admit_range(solid_ctx* ctx, uint64_t lo, uint64_t hi, cudaStream_t s) {
+  if (ctx->epoch + 1 > kMaxEpoch) {
+    solid_status rc = init_scratch(ctx, s);
+    if (rc != SOLID_OK) return rc;
+  }
+  ++ctx->epoch;
+  KParams& kp = ctx->kp;
+  kp.epoch = ctx->epoch;
+  kp.salt = splitmix64(0x5A17ull ^ ((unsigned long long)ctx->epoch << 20));
+  kp.j_lo = lo;
+  kp.n = hi;
+  CK(cudaMemsetAsync(ctx->st, 0, kStHead, s));
+  CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
+  CK(cudaEventRecord(ctx->ev[0], s));
+  CK(launch_hash(kp, s, lo, hi));
+  ctx->launches = 1;
+  solid_status rc = lookup_resolve(ctx, s);
+  if (rc != SOLID_OK) return rc;
+  return solid_insert_batch(ctx, s);
 }
 
 extern "C" solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch,
@@ -1836,7 +1872,7 @@ extern "C" solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* bat
   set_slot(ctx, (ctx->head + ctx->outstanding) % kRing);
   solid_status rc = do_lookup(ctx, batch, out, stream);
   if (rc != SOLID_OK) return rc;
-  rc = enqueue_commit(ctx, (cudaStream_t)stream, true);
+  rc = enqueue_commit(ctx, (cudaStream_t)stream);
   ctx->pending = false;
   if (rc != SOLID_OK) return rc;
   ++ctx->outstanding;
@@ -1876,24 +1912,28 @@ __global__ void __launch_bounds__(256) k_widen16(const uint16_t* in, uint32_t* o
   if (blockIdx.x == 0 && threadIdx.x < (T & 7)) out[8 * n8 + threadIdx.x] = in[8 * n8 + threadIdx.x];
 }
 
-// offsets of a sub-batch rebased to 0
-__global__ void k_rebase(const uint64_t* in, uint64_t* out, uint64_t m) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) out[i] = in[i] - in[0];
-}
-
 // Host-buffer admission: batch arrays copied in (tokens as 32- or 16-bit ids), lookup + insert,
-// results copied out; synchronises the stream.
+// results copied out; synchronises the stream.  The batch is validated on the host first
+// (offsets, sizes), so a rejected batch never starts; it is admitted as ONE batch (all or
+// nothing, R9) — only K_A is split: the tokens are copied in kHostChunks pieces on a second
+// stream and each piece's requests are hashed as soon as their tokens have arrived, so the
+// copies overlap the hashing; one resolver and one commit follow.
 static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* tokens,
                                       int token_bytes, const uint64_t* offsets,
                                       const uint32_t* users, const uint8_t* enforce,
                                       solid_result* out_host, void* stream) {
   if (!ctx) return SOLID_ERR_INVALID;
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
+  if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "admit_host with a pending lookup");
+  solid_status rc = require_collected(ctx, "admit_host");
+  if (rc != SOLID_OK) return rc;
   if (!offsets || (n && (!tokens || !users || !out_host)))
     return fail(ctx, SOLID_ERR_INVALID, "null batch pointer");
   if (n > ctx->cfg.max_batch_requests)
     return fail(ctx, SOLID_ERR_INVALID, "n_requests > max_batch_requests");
+  if (offsets[0] != 0) return fail(ctx, SOLID_ERR_INVALID, "invalid batch: offsets[0] != 0");
+  for (uint64_t j = 0; j < n; ++j)
+    if (offsets[j + 1] < offsets[j]) return fail(ctx, SOLID_ERR_INVALID, "invalid batch: offsets");
   const uint64_t T = offsets[n];
   if (T > ctx->cfg.max_batch_tokens) return fail(ctx, SOLID_ERR_INVALID, "tokens > max_batch_tokens");
   CK(cudaSetDevice(ctx->dev));
@@ -1911,14 +1951,11 @@ static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* to
   CK(cudaMemcpyAsync(ctx->h_offsets, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
   if (n) CK(cudaMemcpyAsync(ctx->h_users, users, n * 4, cudaMemcpyHostToDevice, s));
   if (n && enforce) CK(cudaMemcpyAsync(ctx->h_enforce, enforce, n, cudaMemcpyHostToDevice, s));
-  // Large batches are admitted as kHostChunks consecutive sub-batches (identical results,
-  // reading R1) so the token copy of chunk k+1 (copy stream) overlaps the admission of chunk k.
   const uint32_t K = (T * (uint64_t)token_bytes >= (64ull << 20) && n >= 4 * kHostChunks &&
-                      !ctx->ev_state && !ctx->pool) ? kHostChunks : 1u;
+                      !ctx->ev_state) ? kHostChunks : 1u;
   if (K > 1 && !ctx->s_copy) {
     CK(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
     for (auto& e : ctx->ev_chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(cudaMalloc(&ctx->h_offs_sub, (ctx->cfg.max_batch_requests + kHostChunks + 1) * 8));
   }
   cudaStream_t sc = K > 1 ? ctx->s_copy : s;
   if (K > 1) {                       // the copy stream starts after the small copies were enqueued
@@ -1933,35 +1970,37 @@ static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* to
                          cudaMemcpyHostToDevice, sc));
     if (K > 1) CK(cudaEventRecord(ctx->ev_chunk[k], sc));
   }
-  solid_status rc = SOLID_OK;
-  for (uint32_t k = 0; k < K; ++k) {
-    const uint64_t lo = n * k / K, hi = n * (k + 1) / K;
-    const uint64_t a = offsets[lo], b = offsets[hi];
-    if (K > 1) CK(cudaStreamWaitEvent(s, ctx->ev_chunk[k], 0));
-    if (token_bytes == 2 && b > a) {   // widen from an 8-aligned start (earlier ids: same values)
-      const uint64_t a8 = a & ~7ull;
-      k_widen16<<<(unsigned)std::min<uint64_t>(((b - a8) / 8 + 255) / 256 + 1, 8192), 256, 0, s>>>(
-          ctx->h_tokens16 + a8, ctx->h_tokens + a8, b - a8);
-      CK(cudaGetLastError());
+  solid_batch db;
+  db.n_requests = n;
+  db.tokens = ctx->h_tokens;
+  db.offsets = ctx->h_offsets;
+  db.users = ctx->h_users;
+  db.enforce = enforce ? ctx->h_enforce : nullptr;
+  set_slot(ctx, ctx->head);
+  rc = lookup_setup(ctx, &db, ctx->h_out, stream);
+  if (rc == SOLID_OK && ctx->ev_state) {          // evict mode: one piece (K == 1)
+    if (token_bytes == 2 && T)
+      k_widen16<<<(unsigned)std::min<uint64_t>((T / 8 + 255) / 256 + 1, 8192), 256, 0, s>>>(
+          ctx->h_tokens16, ctx->h_tokens, T);
+    rc = evict_lookup(ctx, s);
+  } else if (rc == SOLID_OK) {
+    CK(cudaEventRecord(ctx->ev[0], s));
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint64_t lo = n * k / K, hi = n * (k + 1) / K;
+      const uint64_t a = offsets[lo], b = offsets[hi];
+      if (K > 1) CK(cudaStreamWaitEvent(s, ctx->ev_chunk[k], 0));
+      if (token_bytes == 2 && b > a) {   // widen from an 8-aligned start (earlier ids: same values)
+        const uint64_t a8 = a & ~7ull;
+        k_widen16<<<(unsigned)std::min<uint64_t>(((b - a8) / 8 + 255) / 256 + 1, 8192), 256, 0, s>>>(
+            ctx->h_tokens16 + a8, ctx->h_tokens + a8, b - a8);
+        CK(cudaGetLastError());
+      }
+      CK(launch_hash(ctx->kp, s, lo, hi));
+      ++ctx->launches;
     }
-    solid_batch db;
-    db.n_requests = hi - lo;
-    db.tokens = ctx->h_tokens + a;
-    if (K > 1) {
-      uint64_t* sub = ctx->h_offs_sub + lo + k;
-      k_rebase<<<(unsigned)((hi - lo + 1 + 255) / 256), 256, 0, s>>>(ctx->h_offsets + lo, sub,
-                                                                      hi - lo + 1);
-      CK(cudaGetLastError());
-      db.offsets = sub;
-    } else {
-      db.offsets = ctx->h_offsets;
-    }
-    db.users = ctx->h_users + lo;
-    db.enforce = enforce ? ctx->h_enforce + lo : nullptr;
-    rc = solid_lookup_batch(ctx, &db, ctx->h_out + lo, stream);
-    if (rc == SOLID_OK) rc = solid_insert_batch(ctx, stream);
-    if (rc != SOLID_OK) break;
+    rc = lookup_resolve(ctx, s);
   }
+  if (rc == SOLID_OK) rc = solid_insert_batch(ctx, stream);
   if (K > 1) cudaStreamSynchronize(sc);       // no copy may outlive a failed call
   if (rc != SOLID_OK) return rc;
   if (n) CK(cudaMemcpyAsync(out_host, ctx->h_out, n * sizeof(solid_result), cudaMemcpyDeviceToHost, s));
@@ -1990,6 +2029,15 @@ extern "C" solid_status solid_debug_set_epoch(solid_ctx* ctx, uint32_t epoch) {
   if (!ctx || epoch > kMaxEpoch) return SOLID_ERR_INVALID;
   if (ctx->pending || ctx->outstanding) return fail(ctx, SOLID_ERR_STATE, "batch in flight");
   ctx->epoch = epoch;
+  return SOLID_OK;
+}
+
+// Test hook: the resolver's round limit (default 4093).  A batch that does not converge within
+// it is admitted in parts by the synchronous paths (solid_insert_batch, solid_admit_host).
+extern "C" solid_status solid_debug_set_max_rounds(solid_ctx* ctx, uint32_t rounds) {
+  if (!ctx || rounds < 2 || rounds > kMaxRounds) return SOLID_ERR_INVALID;
+  if (ctx->pending || ctx->outstanding) return fail(ctx, SOLID_ERR_STATE, "batch in flight");
+  ctx->max_rounds = rounds;
   return SOLID_OK;
 }
 
@@ -2027,6 +2075,8 @@ extern "C" solid_status solid_block_keys(solid_ctx* ctx, unsigned long long* key
   if (!ctx || !keys_out) return SOLID_ERR_INVALID;
   if (ctx->dist) return fail(ctx, SOLID_ERR_STATE, "block_keys: not available on a shard");
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "block_keys with a pending lookup");
+  if (ctx->split_last)
+    return fail(ctx, SOLID_ERR_STATE, "block_keys: the last batch was committed in parts");
   if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
   CK(cudaSetDevice(ctx->dev));
   cudaStream_t s = (cudaStream_t)stream;

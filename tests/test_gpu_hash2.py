@@ -58,3 +58,28 @@ def test_two_components_with_eviction():
     assert np.array_equal(got, o.process(s))
     gd, ed = idx.dump_ex(), o.dump_ex()
     assert all(np.array_equal(gd[f], ed[f]) for f in ["key", "owner", "sharer", "last_used"])
+
+
+@pytest.mark.parametrize("components,reuse", [(1, 2), (2, 1)])
+def test_constructed_collision(components, reuse):
+    """The CUDA path on the constructed H-def v2 collision (tests/hash_collide.py): one-component
+    keys give user 2 a false hit on user 1's block 2, two-component keys do not — equal to the
+    oracle, results and index."""
+    import torch
+    import paper_2603_10726_b200 as P
+    from hash_collide import colliding_seed_and_prompts
+    from workloads.gen import _pack
+    blk1 = np.arange(16, dtype=np.uint32) * 101 + 3
+    seed, pa, pb = colliding_seed_and_prompts(blk1, tail_len=5)
+    s = _pack("collide", [pa, pb, pb, pa], [1, 2, 3, 3])
+    for policy in ("apc", "solidarity"):
+        idx = P.Index(policy, capacity_blocks=1024, max_batch_tokens=s.n_tokens + 64,
+                      max_batch_requests=8, seed=seed, hash_components=components)
+        got = P.as_numpy(idx.admit(**P.to_device(s)))
+        torch.cuda.synchronize()
+        o = Oracle(16, seed, POL[policy], components=components)
+        exp = o.process(s)
+        assert np.array_equal(got, exp)
+        assert int(got["reused"][1]) == reuse
+        gd, ed = idx.dump(), o.dump()
+        assert all(np.array_equal(gd[f], ed[f]) for f in ["key", "owner", "sharer"])

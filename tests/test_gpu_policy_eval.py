@@ -49,7 +49,7 @@ def test_theta_sweep_closed_loop(theta):
     import paper_2603_10726_b200 as P
     s = two_level("W4")
     admit, _ = _gpu_admit("solidarity", s)
-    act = P.Activator(theta=theta, window_len=256, min_samples=2, grid=512,
+    act = P.Activator(theta=theta, window_len=256, min_samples=16, grid=512,
                       max_samples=s.n_requests + 1, max_queries=64)
     dev = lambda a, t: torch.from_numpy(np.ascontiguousarray(a)).to(dtype=t, device="cuda")
     overl = []

@@ -117,6 +117,10 @@ def test_isolation_active_rules():
     assert isolation_active(np.array([]), np.array([]), ActivatorConfig())[0]
     assert isolation_active(a[:1], b, ActivatorConfig())[0]
     assert isolation_active(a[:4], b, ActivatorConfig(min_samples=5))[0]
+    # SPEC S:282 default min_samples = 16: 15 samples in a class keep the fail-safe on, 16 do not
+    assert ActivatorConfig().min_samples == 16
+    assert isolation_active(a[:15], b, ActivatorConfig(theta=0.0))[0]
+    assert not isolation_active(a[:16], b, ActivatorConfig(theta=0.0))[0]
     assert not isolation_active(a, b, ActivatorConfig(theta=0.0))[0]
     en, ov = isolation_active(a, b, ActivatorConfig(theta=1.0))
     assert ov < 1.0 and en

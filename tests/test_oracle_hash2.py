@@ -77,3 +77,57 @@ def test_decisions_do_not_depend_on_the_key_function(policy):
         assert len(da) == len(db)
         assert sorted(zip(da["owner"], da["sharer"])) == sorted(zip(db["owner"], db["sharer"]))
         assert not np.array_equal(np.sort(da["key"]), np.sort(db["key"]))
+
+
+def test_unsplitmix_inverts_splitmix():
+    from hash_collide import splitmix64, unsplitmix64
+    rng = np.random.default_rng(11)
+    for x in rng.integers(0, 1 << 63, size=500, dtype=np.uint64).tolist() + [0, 1, MASK]:
+        assert unsplitmix64(splitmix64(x)) == x
+        assert splitmix64(x) == Oracle.splitmix64(x)
+
+
+def _prompt_stream(prompts, users):
+    from workloads.gen import _pack
+    return _pack("collide", list(prompts), list(users))
+
+
+def test_constructed_chain_collision_separated_by_second_component():
+    """key2_of pinned by construction (not by retyping it): two prompts whose FIRST chain values
+    are equal at depth 2 (a collision built from the secret base, tests/hash_collide.py) must get
+    equal H-def v2 keys — a false prefix hit, user 2 reusing user 1's block 2 under APC — and
+    different H-def v3 keys, so the second component (S2) must enter the key: a key2_of that
+    dropped S2, or mixed it so that it cancels, fails here."""
+    from hash_collide import colliding_seed_and_prompts
+    blk1 = np.arange(16, dtype=np.uint32) * 101 + 3
+    seed, pa, pb = colliding_seed_and_prompts(blk1, tail_len=5)
+    o1 = Oracle(16, seed, POLICY_APC)
+    o2 = Oracle(16, seed, POLICY_APC, components=2)
+    Sa, Ka = o1.chain(pa)
+    Sb, Kb = o1.chain(pb)
+    assert Sa[0] == Sb[0] and Sa[1] == Sb[1] and Ka[1] == Kb[1]       # the built collision
+    S1a, S2a, K2a = o2.chain2(pa)
+    S1b, S2b, K2b = o2.chain2(pb)
+    assert S1a[1] == S1b[1] and S2a[1] != S2b[1]                       # only S2 tells them apart
+    assert K2a[0] == K2b[0] and K2a[1] != K2b[1]
+    # consequence for the method (P:102-104 longest cached prefix): one-component keys serve
+    # user 2 user 1's block 2 (content it never sent); two-component keys do not
+    s = _prompt_stream([pa, pb], [1, 2])
+    assert o1.process(s)["reused"].tolist() == [0, 2]
+    assert o2.process(s)["reused"].tolist() == [0, 1]
+
+
+def test_key2_recovers_second_chain_by_inversion():
+    """The key is an invertible function of (S, S2): undoing fmix64 (its independently derived
+    inverse, test_oracle_hash._unfmix), the offset, the XOR with S and the odd multiplier gives
+    back S2 — the closed-form second polynomial — for every depth."""
+    from test_oracle_hash import _unfmix
+    o = Oracle(16, 0x5011D000, POLICY_APC, components=2)
+    rng = np.random.default_rng(4)
+    inv_mix = pow(0x9E3779B97F4A7C15, -1, 1 << 64)
+    for _ in range(6):
+        toks = rng.integers(0, 1 << 20, size=16 * int(rng.integers(1, 9)), dtype=np.uint32)
+        S, S2, K = o.chain2(toks, int(rng.integers(0, 1 << 31)), -1)
+        for b in range(len(K)):
+            x = (_unfmix(int(K[b])) - 0x9E3779B97F4A7C15) & MASK
+            assert ((x ^ int(S[b])) * inv_mix) & MASK == int(S2[b])

@@ -61,8 +61,8 @@ def test_two_level_sharing_costs_reuse_between_the_baselines():
         assert ui < cs < apc, (w, ui, cs, apc)
 
 
-def _sweep_point(s, theta):
-    cfg = ActivatorConfig(theta=float(theta))
+def _sweep_point(s, theta, **kw):
+    cfg = ActivatorConfig(theta=float(theta), **kw)
     o = Oracle(16, SEED, POLICY_SOLIDARITY)
     act = lambda tt, pt, fr, cuts: enforce_stream(tt, pt, fr, cuts, cfg)[0]
     return closed_loop(s, lambda b: o.process(b), act, batch=50)
@@ -71,13 +71,15 @@ def _sweep_point(s, theta):
 def test_theta_sweep_endpoints_and_trend():
     """§6.3 / fig:kde_threshold_results: θ = 0 gives Prefix Caching's
     reuse request by request (isolation never enforced once windows exist, flags still written),
-    θ = 1 the detector-always-on reuse; the hit rate is non-increasing in θ up to 1 point."""
+    θ = 1 the detector-always-on reuse; the hit rate is non-increasing in θ up to 1 point.
+    min_samples = 2 here, so the fail-safe (R21) covers only the first batch and θ = 0 equals
+    Prefix Caching request by request; the SPEC default (16) is covered below."""
     s = two_level("W4")
     apc = _run(s, POLICY_APC)
     always = _run(s, POLICY_SOLIDARITY)
     hr = []
     for th in np.linspace(0.0, 1.0, 11):
-        res, en, _ = _sweep_point(s, th)
+        res, en, _ = _sweep_point(s, th, min_samples=2)
         hr.append(hit_rate(res))
         if th == 0.0:
             assert np.array_equal(res["reused"], apc["reused"])
@@ -86,3 +88,16 @@ def test_theta_sweep_endpoints_and_trend():
             assert np.array_equal(res["reused"], always["reused"]) and en.all()
     assert hr[0] > hr[-1]
     assert all(b <= a + 0.01 for a, b in zip(hr, hr[1:])), hr
+
+
+def test_theta_zero_default_min_samples_failsafe_only():
+    """SPEC S:266 / S:282 (min_samples = 16): with θ = 0 a request is enforced exactly while one
+    of its windows holds fewer than 16 samples (fail-safe), never after both have 16."""
+    s = two_level("W4")
+    res, en, (tt, pt, fr) = _sweep_point(s, 0.0)
+    hit = np.concatenate([[0], np.cumsum(fr >= 0.8)])
+    miss = np.concatenate([[0], np.cumsum(fr <= 0.2)])
+    cut = (np.arange(s.n_requests) // 50) * 50            # samples completed before the batch
+    failsafe = (np.minimum(hit[cut], 256) < 16) | (np.minimum(miss[cut], 256) < 16)
+    assert failsafe[:50].all()
+    assert np.array_equal(en.astype(bool), failsafe)
