@@ -497,6 +497,99 @@ def measure_configs(dev, args):
     return out
 
 
+def c5_exact_properties(timed, got):
+    """Per-request values C5's structure fixes (workloads/c5.py), checked on the timed batch:
+    a continuing conversation reuses exactly its cached history prefix (floor(prefix / 16): the
+    next block holds its own new message); a new session reuses exactly its 32-block system
+    prompt, diverted there (flagged since the warm phase); an attacker's first probe
+    reuses 32 blocks and every later one 47 (its own isolated copy of the victim's profile), and
+    no probe reuses the block holding the victim's secret token."""
+    U = timed.meta["users"]
+    segs = np.diff(timed.ptr)
+    attacker = timed.users >= U
+    new = (segs == 2) & ~attacker
+    cont = ~new & ~attacker
+    seg_end = np.concatenate([[0], np.cumsum(timed.length)])
+    prefix = seg_end[timed.ptr[1:] - 1] - seg_end[timed.ptr[:-1]]
+    r = got["reused"].astype(np.int64)
+    ai = np.nonzero(attacker)[0]
+    first = np.zeros(ai.size, bool)
+    first[np.unique(timed.users[ai], return_index=True)[1]] = True
+    bad = {"continuing": int((r[cont] != prefix[cont] // 16).sum()),
+           "new_session": int(((r[new] != 32) | (got["divert_at"][new] != 32)).sum()),
+           "probe_first": int((r[ai][first] != 32).sum()),
+           "probe_later": int((r[ai][~first] != 47).sum()),
+           "probe_hit_secret": int((r[ai] >= 48).sum())}
+    return {"status": "exact" if not any(bad.values()) else "MISMATCH", "violations": bad,
+            "requests_checked": int(cont.sum() + new.sum() + ai.size),
+            "what": "every request of the timed batch against the reuse its structure fixes"}
+
+
+def measure_c5(dev, args):
+    """BASELINE configs[4] C5 on ONE GPU (one B200 holds it): warm phase (200 000
+    users' conversations, ~1.06e8 entries) admitted untimed, index checkpointed; one step = the
+    4 000 000-request batch (4.2e9 tokens, 16.9 GB of token ids) admitted with
+    solid_admit_batch; the index restored to the warm state before every step (outside the
+    events).  Tokens are generated on the device (workloads/c5.py materialize_torch)."""
+    import torch
+    import paper_2603_10726_b200 as P
+    from workloads.c5 import c5_large
+    t0 = time.perf_counter()
+    warm, timed = c5_large(scale=1.0)
+    cap = warm.n_blocks() + timed.n_blocks() // 4 + (1 << 16)
+    idx = P.Index("solidarity", capacity_blocks=cap,
+                  max_batch_tokens=max(warm.n_tokens, timed.n_tokens) + 64,
+                  max_batch_requests=max(warm.n_requests, timed.n_requests), seed=SEED,
+                  device=dev.index or 0, max_blocks=1024)
+    wt, wo, wu = warm.materialize_torch(dev)
+    idx.admit(wt, wo, wu, None)
+    torch.cuda.synchronize()
+    live0 = idx.stats()["live_entries"]
+    del wt, wo, wu
+    torch.cuda.empty_cache()
+    idx.checkpoint()
+    tt, to, tu = timed.materialize_torch(dev)
+    out = torch.empty((timed.n_requests, 6), dtype=torch.int32, device=dev)
+    setup_s = time.perf_counter() - t0
+    cs = torch.cuda.current_stream(dev)
+    ms, st = [], None
+    for k in range(1 + max(args.steps // 10, 3)):
+        idx.restore()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        idx.admit_async(tt, to, tu, None, out=out)
+        e1.record(cs)
+        idx.status()
+        if k >= 1:
+            ms.append(e0.elapsed_time(e1))
+            st = idx.stats()
+    med = statistics.median(ms)
+    got = P.as_numpy(out)
+    nblk = timed.n_blocks()
+    r = {"workload": f"c5_large: warm {warm.n_requests} conversations -> {live0} entries "
+                     f"(untimed); timed = ONE batch of {timed.n_requests} requests "
+                     f"({timed.n_tokens} tokens, {nblk} blocks): "
+                     f"{timed.meta['continuing']} continuing, {timed.meta['new_sessions']} new "
+                     f"sessions, {timed.meta['probes']} probes",
+         "n_gpus": 1, "ms_per_batch": med, "ms_all": ms,
+         "requests_per_s": timed.n_requests / (med / 1e3), "blocks_per_s": nblk / (med / 1e3),
+         "resolver_rounds": st["last_rounds"],
+         "phases_ms": {"hash": st["ms_hash"], "resolve": st["ms_resolve"],
+                       "commit": st["ms_commit"]},
+         "round_us": st["round_us"], "algorithmic_bytes": st["algorithmic_bytes"],
+         "whole_step_hbm_frac": st["algorithmic_bytes"] / (med / 1e3) / 1e9 / _peaks()[0],
+         "hash_kernel_hbm_frac": (64 * nblk + 12 * timed.n_requests + 16 * st["last_shared_keys"])
+                                 / (st["ms_hash_kernel"] / 1e3) / 1e9 / _peaks()[0],
+         "live_entries_before": live0, "inserted": st["last_inserted"],
+         "index_slots": int(1 << (2 * cap - 1).bit_length()),
+         "parity": c5_exact_properties(timed, got), "setup_s": setup_s,
+         "hit_rate": float(got["reused"].sum() / max(got["n_blocks"].sum(), 1))}
+    del idx, tt, to, tu, out
+    torch.cuda.empty_cache()
+    return r
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -696,6 +789,7 @@ def main():
     ap.add_argument("--no-evict", action="store_true")
     ap.add_argument("--no-policy-eval", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
@@ -913,6 +1007,11 @@ def main():
     other = None
     if rank == 0 and world == 1 and not args.profile and not args.no_configs:
         other = measure_configs(dev, args)
+        if not args.no_c5:
+            try:
+                other["c5"] = measure_c5(dev, args)
+            except Exception as e:   # reported, never silently dropped
+                other["c5"] = {"error": f"{type(e).__name__}: {e}"}
 
     peval = None
     if rank == 0 and world == 1 and not args.profile and not args.no_policy_eval:

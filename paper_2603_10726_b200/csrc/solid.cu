@@ -1131,17 +1131,41 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
   }
   const bool ok = live && !st->err && !(n && st->conv == 0);
   if (ok) {                            // new entries (a[6]) and new sharer writes (a[7])
+    // flat index over every registered id: segment prefix sums in shared memory, so each thread
+    // handles ~ids / threads ids with independent loads (no per-segment serial loop)
+    __shared__ uint32_t s_pre[kNSeg + 1];
+    if (threadIdx.x < kNSeg) s_pre[threadIdx.x + 1] = min(seg[threadIdx.x].v, kp.seg_cap);
+    if (threadIdx.x == 0) s_pre[0] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int q = 1; q <= kNSeg; ++q) s_pre[q] += s_pre[q - 1];
+    __syncthreads();
     const uint32_t tf = final_round(kp);
     const int W = (int)(tf & 1);
     const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
+    const uint32_t total = s_pre[kNSeg];
+    constexpr int UQ = 4;                    // ids per thread per step, loads in flight together
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t sg = 0; sg < (uint32_t)kNSeg; ++sg) {
-      const uint32_t cnt = min(seg[sg].v, kp.seg_cap);
-      for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += stride) {
-        const ulonglong2 pw = ldw128(&kp.hot[sg * kp.seg_cap + x + 1].v[2 * W]);
-        const uint32_t itag = (uint32_t)(pw.x >> 32);
+    for (uint32_t g0 = blockIdx.x * blockDim.x + threadIdx.x; g0 < total; g0 += UQ * stride) {
+      ulonglong2 pw[UQ];
+#pragma unroll
+      for (int q = 0; q < UQ; ++q) {
+        const uint32_t g = g0 + q * stride;
+        pw[q] = make_ulonglong2(0ull, 0ull);
+        if (g < total) {
+          uint32_t lo = 0, hi = kNSeg;       // segment: s_pre[lo] <= g < s_pre[lo + 1]
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_pre[mid] <= g) lo = mid; else hi = mid;
+          }
+          pw[q] = ldw128(&kp.hot[lo * kp.seg_cap + (g - s_pre[lo]) + 1].v[2 * W]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UQ; ++q) {
+        const uint32_t itag = (uint32_t)(pw[q].x >> 32);
         a[6] += itag == tag;
-        a[7] += itag == tagS && (uint32_t)(pw.y >> 32) == tag;
+        a[7] += itag == tagS && (uint32_t)(pw[q].y >> 32) == tag;
       }
     }
   }
@@ -1429,9 +1453,13 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   ctx->tcap = next_pow2(std::max<uint64_t>((cfg->evict ? 4 : 2) * cfg->capacity_blocks, 1024));
   ctx->slot_cap = cfg->max_batch_tokens / kBS + 1;
   // distinct keys per batch <= Shared keys + isolated keys of every divert depth tried; ids are
-  // allocated from kNSeg segments chosen by request, each with 2x headroom over an even share
+  // allocated from kNSeg segments chosen by request (j mod kNSeg), each with headroom over an
+  // even share: 2x for small batches, 1.25x once a segment's share is large (the requests of a
+  // big batch spread evenly; C5's 4e9 tokens would otherwise need 60 GB of id state)
   ctx->idcap = std::max<uint64_t>(2 * ctx->slot_cap, 1u << 16);
-  ctx->seg_cap = (uint32_t)std::min<uint64_t>(2 * ctx->idcap / kNSeg + 1024, 0x7FFFFFFFull);
+  const uint64_t share = ctx->idcap / kNSeg;
+  ctx->seg_cap = (uint32_t)std::min<uint64_t>(
+      (share >= (1u << 20) ? share + share / 4 : 2 * share) + 1024, 0x7FFFFFFFull);
   ctx->idcap = (uint64_t)kNSeg * ctx->seg_cap + 1;
   ctx->scap = next_pow2(2 * ctx->idcap);
   if (ctx->tcap > (1ull << 32) || ctx->idcap > (1ull << 32)) {   // 32-bit slot / id indices
@@ -1719,7 +1747,7 @@ static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s) {
   if (n) {
     if (ctx->kp.pool_cnt) CK(cudaMemsetAsync(ctx->kp.pool_cnt, 0, ctx->kp.n * 4, s));
     // counts and the capacity decision first (device-resident live count), then the claims
-    k_stats<<<std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(
+    k_stats<<<1184, 256, 0, s>>>(   // 148 SMs x 8: the id count spans every registered key
         ctx->kp.out + ctx->kp.j_lo, n, ctx->st, ctx->live_dev, ctx->cfg.capacity_blocks,
         ctx->seg_cnt, ctx->kp);
     CK(cudaGetLastError());
