@@ -497,34 +497,6 @@ def measure_configs(dev, args):
     return out
 
 
-def c5_exact_properties(timed, got):
-    """Per-request values C5's structure fixes (workloads/c5.py), checked on the timed batch:
-    a continuing conversation reuses exactly its cached history prefix (floor(prefix / 16): the
-    next block holds its own new message); a new session reuses exactly its 32-block system
-    prompt, diverted there (flagged since the warm phase); an attacker's first probe
-    reuses 32 blocks and every later one 47 (its own isolated copy of the victim's profile), and
-    no probe reuses the block holding the victim's secret token."""
-    U = timed.meta["users"]
-    segs = np.diff(timed.ptr)
-    attacker = timed.users >= U
-    new = (segs == 2) & ~attacker
-    cont = ~new & ~attacker
-    seg_end = np.concatenate([[0], np.cumsum(timed.length)])
-    prefix = seg_end[timed.ptr[1:] - 1] - seg_end[timed.ptr[:-1]]
-    r = got["reused"].astype(np.int64)
-    ai = np.nonzero(attacker)[0]
-    first = np.zeros(ai.size, bool)
-    first[np.unique(timed.users[ai], return_index=True)[1]] = True
-    bad = {"continuing": int((r[cont] != prefix[cont] // 16).sum()),
-           "new_session": int(((r[new] != 32) | (got["divert_at"][new] != 32)).sum()),
-           "probe_first": int((r[ai][first] != 32).sum()),
-           "probe_later": int((r[ai][~first] != 47).sum()),
-           "probe_hit_secret": int((r[ai] >= 48).sum())}
-    return {"status": "exact" if not any(bad.values()) else "MISMATCH", "violations": bad,
-            "requests_checked": int(cont.sum() + new.sum() + ai.size),
-            "what": "every request of the timed batch against the reuse its structure fixes"}
-
-
 def measure_c5(dev, args):
     """BASELINE configs[4] C5 on ONE GPU (one B200 holds it): warm phase (200 000
     users' conversations, ~1.06e8 entries) admitted untimed, index checkpointed; one step = the
@@ -534,6 +506,8 @@ def measure_c5(dev, args):
     import torch
     import paper_2603_10726_b200 as P
     from workloads.c5 import c5_large
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from c5_props import c5_check        # the per-request values C5's structure fixes
     t0 = time.perf_counter()
     warm, timed = c5_large(scale=1.0)
     cap = warm.n_blocks() + timed.n_blocks() // 4 + (1 << 16)
@@ -583,7 +557,7 @@ def measure_c5(dev, args):
                                  / (st["ms_hash_kernel"] / 1e3) / 1e9 / _peaks()[0],
          "live_entries_before": live0, "inserted": st["last_inserted"],
          "index_slots": int(1 << (2 * cap - 1).bit_length()),
-         "parity": c5_exact_properties(timed, got), "setup_s": setup_s,
+         "parity": c5_check(timed, got), "setup_s": setup_s,
          "hit_rate": float(got["reused"].sum() / max(got["n_blocks"].sum(), 1))}
     del idx, tt, to, tu, out
     torch.cuda.empty_cache()

@@ -2,16 +2,11 @@
 
 * reduced scale (0.1: 20 000 users, ~1.1e7 warm entries, a 400 000-request timed batch): the
   CUDA path against the oracle, every result field and the whole index;
-* full scale on ONE GPU (200 000 users, ~1.06e8 warm entries, ONE 4 000 000-request batch of
-  4.2e9 tokens): properties that fix every result of the batch without the oracle —
-    - a continuing conversation reuses exactly its cached history prefix: r = floor(prefix/16)
-      (the block after it holds the new message, which no other request contains);
-    - a new session reuses exactly its 32-block system prompt and is diverted there (its end is
-      flagged since the warm phase: P:457-459, R7);
-    - an attacker's first probe reuses the 32 system-prompt blocks, every later probe of the
-      same attacker 47 (its own isolated copy of the victim's profile), and NO probe ever
-      reuses the block that holds the victim's secret token (the §5 guarantee, P:566-572);
-  and R1 at full size: the same batch admitted as 4 consecutive parts gives identical results
+* full scale on ONE GPU (200 000 users, ~1.02e8 warm entries, ONE 4 000 000-request batch of
+  4.2e9 tokens): the per-request values C5's structure fixes (tests/c5_props.py: continuing
+  conversations reuse their cached prefix, new sessions divert at the flagged system prompt,
+  no probe is ever served beyond the system prompt — the §5 guarantee) for every request, and
+  R1 at full size: the same batch admitted as 4 consecutive parts gives identical results
   and an identical index;
 * the sharded protocol (loopback, G = 8 shards on one GPU) at reduced scale against the oracle.
 A full-size oracle comparison runs with SOLID_C5_ORACLE=1 (host RAM ~40 GB, ~3 min).
@@ -21,6 +16,7 @@ import os
 import numpy as np
 import pytest
 
+from c5_props import c5_check
 from oracle import Oracle
 from workloads.c5 import c5_large
 
@@ -78,32 +74,7 @@ def test_c5_reduced_scale_oracle_parity():
     got = _admit_dev(idx, timed, asynchronous=True)
     exp, ed = _oracle(warm, timed)
     _same(got, exp, idx.dump(), ed, "c5 x0.1")
-
-
-def _expected_properties(timed, got):
-    """The exact per-request values that C5's structure fixes (module docstring)."""
-    kinds = np.full(timed.n_requests, -1, np.int8)
-    segs = np.diff(timed.ptr)
-    offs = timed.offsets().astype(np.int64)
-    lens = np.diff(offs)
-    U = timed.meta["users"]
-    attacker = timed.users >= U
-    new = (segs == 2) & ~attacker
-    cont = ~new & ~attacker
-    # continuing: the history prefix = every segment but the last (the new message)
-    seg_end = np.concatenate([[0], np.cumsum(timed.length)])
-    prefix = seg_end[timed.ptr[1:] - 1] - seg_end[timed.ptr[:-1]]
-    r = got["reused"].astype(np.int64)
-    assert np.array_equal(r[cont], prefix[cont] // 16), "continuing: reuse != cached prefix"
-    assert (r[new] == 32).all() and (got["divert_at"][new] == 32).all()
-    # probes, per attacker in batch order: 32 first, then 47; never the secret block (48)
-    ai = np.nonzero(attacker)[0]
-    first = np.zeros(ai.size, bool)
-    _, idx_first = np.unique(timed.users[ai], return_index=True)
-    first[idx_first] = True
-    assert (r[ai][first] == 32).all() and (r[ai][~first] == 47).all()
-    assert (r[ai] < 48).all()
-    return int(cont.sum()), int(new.sum()), int(ai.size)
+    assert c5_check(timed, got)["status"] == "exact"
 
 
 def test_c5_full_size_single_gpu():
@@ -118,8 +89,9 @@ def test_c5_full_size_single_gpu():
     idx.checkpoint()
     got = _admit_dev(idx, timed, asynchronous=True)
     st = idx.stats()
-    n_cont, n_new, n_probe = _expected_properties(timed, got)
-    assert (n_cont, n_new, n_probe) == (2_000_000, 1_600_000, 400_000)
+    chk = c5_check(timed, got)
+    assert chk["status"] == "exact", chk
+    assert chk["counts"] == (2_000_000, 1_600_000, 400_000)
     d_one = idx.dump()
     assert len(d_one) == live0 + st["last_inserted"]
     # R1: the same batch as 4 consecutive parts

@@ -135,7 +135,8 @@ def victim_of(history):
     return history[-1][0] if history else 1
 
 
-def _guarantee_run(history, pre, secret, cands, attackers, benign, order):
+def _guarantee_run(history, pre, secret, cands, attackers, benign, order, capacity=0,
+                   victim_between=None):
     """Replay `history` (list of (user, names)), then the probing sequence pre.v_i issued by
     attackers (round robin), interleaved with disjoint benign requests (order = list of 'p'/'b').
     Returns (precondition_holds, literal_precondition, leaked).  A leak is a probe pre.secret whose
@@ -143,7 +144,7 @@ def _guarantee_run(history, pre, secret, cands, attackers, benign, order):
     the attacker's own isolated copies (divert at f <= |pre|) reveals nothing about the victim.
     The premise "c contains pre.secret owned by u" is part of precondition_holds."""
     B = Blocks(seed=77)
-    o = Oracle(16, SEED, POLICY_SOLIDARITY)
+    o = Oracle(16, SEED, POLICY_SOLIDARITY, capacity=capacity)
     for u, names in history:
         o.process_prompts([B.prompt(names)], [u])
     tab = table_as_dict(o)
@@ -158,20 +159,28 @@ def _guarantee_run(history, pre, secret, cands, attackers, benign, order):
     premise = tab.get(int(Ksec[-1]), (None,))[0] == victim_of(history)
     refined = premise and len(pre) >= 1 and (pre_flagged or not child_v1_present)
     literal = premise and len(pre) >= 1 and (pre_flagged or cands[0] != secret)
+    sec_key = int(Ksec[-1])
+    victim = victim_of(history)
     leaked = False
     pi = bi = 0
     for kind in order:
         if kind == "p" and pi < len(cands):
             v = cands[pi]
+            # with eviction the victim's entry may be gone (nothing left to leak) or re-inserted
+            # by someone else: only a probe that serves the VICTIM's pre.secret entry leaks
+            victims_entry = table_as_dict(o).get(sec_key, (None,))[0] == victim
             res = o.process_prompts([B.prompt(pre + [v])], [attackers[pi % len(attackers)]])[0]
             f = int(res["divert_at"])
-            if v == secret and int(res["reused"]) > len(pre) and (f < 0 or f > len(pre)):
+            if (v == secret and victims_entry and int(res["reused"]) > len(pre)
+                    and (f < 0 or f > len(pre))):
                 leaked = True
             pi += 1
         elif kind == "b" and bi < len(benign):
             u, names = benign[bi]
             o.process_prompts([B.prompt(names)], [u])
             bi += 1
+        elif kind == "v" and victim_between is not None:
+            o.process_prompts([B.prompt(victim_between)], [victim])
     return refined, literal, leaked
 
 
@@ -226,6 +235,53 @@ def test_p3_documented_exclusions_leak():
     refined, literal, leaked = _guarantee_run([(1, ["P", "V1"]), (1, ["P", "S"])], ["P"], "S",
                                               ["V1", "S"], [2], [], ["p", "p"])
     assert literal and not refined and leaked
+
+
+@pytest.mark.parametrize("capacity", [3, 4, 6])
+def test_p3_security_guarantee_under_lru_eviction(capacity):
+    """§5 with eviction ("eviction is benign for security"; S:117-125 LRU, flags die with
+    their entry S:120/S:124): the same brute force with a capacity of 3-6 entries and the probes
+    interleaved with disjoint benign requests (which evict), under the premise of P:566-572
+    (probes by non-victims; the victim sends nothing during the probing): no probe ever serves
+    the victim's pre.secret entry while the refined precondition held at the start."""
+    victim, a1, a2, ben = 1, 2, 3, 4
+    alphabet = ["a", "b", "c"]
+    checked = leaks = 0
+    rng = np.random.default_rng(100 + capacity)
+    for hist in _histories(victim, [a1, a2, ben], alphabet, 3, 6):
+        pre = [alphabet[int(rng.integers(3))] for _ in range(int(rng.integers(1, 3)))]
+        secret = alphabet[int(rng.integers(3))]
+        hist = hist + [(victim, pre + [secret])]
+        cands = [c for c in alphabet if c != secret]
+        rng.shuffle(cands)
+        cands = cands + [secret]
+        benign = [(ben, ["d", "e"]), (ben, ["e"]), (ben, ["f", "d"]), (ben, ["g"])]
+        order = list(rng.permutation(["p"] * len(cands) + ["b"] * len(benign)))
+        refined, _, leaked = _guarantee_run(hist, pre, secret, cands, [a1, a2], benign, order,
+                                            capacity=capacity)
+        if refined:
+            checked += 1
+            leaks += leaked
+    assert checked > 800
+    assert leaks == 0
+
+
+def test_p3_eviction_reincarnation_exclusion():
+    """Documented exclusion (3) (R31): outside P:566-572's premise — the VICTIM
+    re-sends pre.secret after eviction removed pre and its flag — every re-cached incarnation of
+    pre is unflagged again, so the attacker gets a fresh first attempt per incarnation (the
+    first-attempt exclusion of P:588-595, repeated).  Witness: capacity 2; the attacker's wrong
+    guess flags P; benign traffic evicts P and S (the flag dies with P); the victim
+    re-sends [P S]; the attacker's next guess, the right one, is served the victim's S."""
+    refined, _, leaked = _guarantee_run(
+        [(1, ["P", "S"])], ["P"], "S", ["X", "S"], [2], [(4, ["d", "e"])], ["p", "b", "v", "p"],
+        capacity=2, victim_between=["P", "S"])
+    assert refined and leaked
+    # the same sequence without the victim's re-request: no leak (the entry is gone)
+    refined, _, leaked = _guarantee_run(
+        [(1, ["P", "S"])], ["P"], "S", ["X", "S"], [2], [(4, ["d", "e"])], ["p", "b", "p"],
+        capacity=2)
+    assert refined and not leaked
 
 
 # ----------------------------------------------------------------------------------------------
