@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SOLID_ABI_VERSION 5u
+#define SOLID_ABI_VERSION 6u
 #define SOLID_USER_NONE 0xFFFFFFFFu   /* "no user": sharer of an unflagged entry */
 
 typedef enum {
@@ -83,6 +83,17 @@ typedef struct {
                                   blocks first, then its new entries take blocks in block order.
                                   See solid_block_table / solid_dump_phys.  Single GPU only;
                                   admission synchronous (solid_admit_batch is refused).          */
+  uint32_t pin;                /* 1 (needs block_table = 1): in-flight pinning (R38; the
+                                  reference count of vLLM's KVCacheBlock beneath P:733).  Every
+                                  admitted request holds one pin on each entry of its block-table
+                                  row until the caller releases that row (solid_release); a pinned
+                                  entry is never evicted — the LRU victim is the smallest
+                                  (last_used, key) among unpinned entries — so its physical block
+                                  is never reclaimed while a running request reads it.  A batch
+                                  one of whose requests would need more victims than there are
+                                  unpinned entries it does not use itself fails with
+                                  SOLID_ERR_CAPACITY, nothing mutated (split it: a single such
+                                  request is refused until pins are released).                   */
 } solid_config;
 
 typedef struct solid_ctx solid_ctx;
@@ -251,6 +262,16 @@ solid_status solid_block_keys(solid_ctx* ctx, unsigned long long* keys_out, void
  * request referenced without being served it and then evicted).  Positions no request's full
  * block covers are not written.  The batch's offsets must still be valid.  Enqueued on stream. */
 solid_status solid_block_table(solid_ctx* ctx, uint32_t* table_out, void* stream);
+
+/* Release one pin on the entry holding each of the n physical block ids in phys (DEVICE array,
+ * e.g. a finished request's block-table row; SOLID_USER_NONE entries are skipped).  pin = 1
+ * contexts only.  Synchronises `stream`; SOLID_ERR_INVALID if some block holds no pinned entry
+ * (those are left unchanged, the others released). */
+solid_status solid_release(solid_ctx* ctx, const uint32_t* phys, uint64_t n, void* stream);
+
+/* Pin count of every physical block (HOST array of capacity_blocks entries; 0 for free blocks).
+ * pin = 1 contexts only. */
+solid_status solid_pins(solid_ctx* ctx, uint32_t* pins_out);
 
 /* Live entries' physical blocks sorted by key (HOST arrays, capacity cap); *n_out = live
  * entries.  block_table = 1 contexts only. */

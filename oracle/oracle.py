@@ -80,6 +80,14 @@ def _load():
         lib.oracle_block_table.argtypes = [vp, vp, u64]
         lib.oracle_dump_phys.restype = u64
         lib.oracle_dump_phys.argtypes = [vp, vp, vp, u64]
+        lib.oracle_set_pin.restype = ctypes.c_int
+        lib.oracle_set_pin.argtypes = [vp, ctypes.c_int]
+        lib.oracle_release.restype = ctypes.c_int
+        lib.oracle_release.argtypes = [vp, vp, u64]
+        lib.oracle_admitted.restype = u64
+        lib.oracle_admitted.argtypes = [vp]
+        lib.oracle_dump_pins.restype = u64
+        lib.oracle_dump_pins.argtypes = [vp, vp, vp, u64]
         _lib = lib
     return _lib
 
@@ -88,11 +96,20 @@ def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
+class PinRefused(ValueError):
+    """A request's eviction step would need a pinned entry (R38): it was refused, nothing of it
+    applied; `admitted` requests of the call before it were admitted."""
+
+    def __init__(self, admitted: int):
+        super().__init__(f"request {admitted} of the call refused: too few unpinned entries")
+        self.admitted = admitted
+
+
 class Oracle:
     """Sequential reference: Oracle(block_size, seed, policy).process(stream) -> results."""
 
     def __init__(self, block_size: int = 16, seed: int = 0, policy: int = POLICY_SOLIDARITY,
-                 capacity: int = 0, components: int = 1, pool: int = 0):
+                 capacity: int = 0, components: int = 1, pool: int = 0, pin: bool = False):
         self.lib = _load()
         self.block_size, self.seed, self.policy = block_size, seed, policy
         self.h = self.lib.oracle_create(block_size, seed & 0xFFFFFFFFFFFFFFFF, policy)
@@ -107,6 +124,8 @@ class Oracle:
         self.pool = pool
         if pool and self.lib.oracle_set_pool(self.h, pool):  # physical blocks (R26-R28)
             raise ValueError("bad pool size")
+        if pin and self.lib.oracle_set_pin(self.h, 1):        # in-flight pinning (R38)
+            raise ValueError("pin needs a pool")
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -128,6 +147,8 @@ class Oracle:
                                       _ptr(en), _ptr(out))
         if err == 4:
             raise ValueError("oracle_process: physical block pool exhausted")
+        if err == 5:
+            raise PinRefused(int(self.lib.oracle_admitted(self.h)))
         if err:
             raise ValueError(f"oracle_process: invalid batch (code {err})")
         return out
@@ -173,6 +194,21 @@ class Oracle:
         k = np.zeros(max(n, 1), dtype=np.uint64)
         p = np.zeros(max(n, 1), dtype=np.uint32)
         self.lib.oracle_dump_phys(self.h, _ptr(k), _ptr(p), n)
+        return k[:n], p[:n]
+
+    def release(self, phys) -> None:
+        """Drop one pin on the entry holding each physical block (NONE entries skipped)."""
+        phys = np.ascontiguousarray(phys, dtype=np.uint32)
+        if self.lib.oracle_release(self.h, _ptr(phys if phys.size else np.zeros(1, np.uint32)),
+                                   phys.size):
+            raise ValueError("oracle_release: a block holds no pinned live entry")
+
+    def dump_pins(self):
+        """(keys, pin counts) of the live entries, sorted by key."""
+        n = self.size()
+        k = np.zeros(max(n, 1), dtype=np.uint64)
+        p = np.zeros(max(n, 1), dtype=np.uint32)
+        self.lib.oracle_dump_pins(self.h, _ptr(k), _ptr(p), n)
         return k[:n], p[:n]
 
     def evictions(self) -> int:

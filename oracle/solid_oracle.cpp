@@ -78,6 +78,7 @@ struct Entry {
   uint64_t last_used; // LRU clock (R22): global sequence number of the last request
                       // that was served this entry or inserted it
   uint32_t phys;      // physical KV block holding the entry's content (R26); NONE = pool off
+  uint32_t pins;      // requests holding the entry's block (R38); > 0: not evictable
 };
 
 struct Ctx {
@@ -107,6 +108,14 @@ struct Ctx {
   std::deque<uint32_t> freeq;
   std::vector<uint64_t> fresh;        // keys the current request inserted, in block order
   std::vector<uint32_t> btab;         // block table of the last oracle_process call (R27)
+  // In-flight pinning (R38, the vLLM KVCacheBlock reference count beneath P:733): with pin on,
+  // every admitted request pins the entries of its block-table row until oracle_release; the
+  // LRU victim is the smallest (last_used, key) among UNPINNED entries, and a request whose
+  // eviction step would find too few of them (other than the entries it uses itself) is
+  // refused before it mutates anything.
+  bool pin;
+  std::vector<uint64_t> key_of_phys;  // physical block -> key of the live entry holding it
+  uint64_t admitted;                  // requests admitted by the last oracle_process call
 };
 
 uint64_t sigma_of(const Ctx& c, uint32_t user) {
@@ -156,7 +165,7 @@ uint32_t owner_of(const Ctx& c, uint64_t key) { return c.table.at(key).owner; }
 // it unchanged — owner, flag and last_used (R8, R23).
 void insert_if_absent(Ctx& c, uint64_t key, uint32_t user, uint64_t seq) {
   if (present(c, key)) return;
-  c.table.emplace(key, Entry{user, (uint32_t)NONE, seq, (uint32_t)NONE});
+  c.table.emplace(key, Entry{user, (uint32_t)NONE, seq, (uint32_t)NONE, 0});
   if (c.capacity) c.lru.insert(std::make_pair(seq, key));
   if (c.pool) c.fresh.push_back(key);
 }
@@ -177,13 +186,32 @@ void touch(Ctx& c, uint64_t key, uint64_t seq) {
 // applied until the invariant holds"; R24).
 void evict_to_capacity(Ctx& c) {
   if (!c.capacity) return;
+  auto victim = c.lru.begin();
   while (c.table.size() > c.capacity) {
-    auto victim = c.lru.begin();
+    while (c.table.at(victim->second).pins) ++victim;    // pinned: not evictable (R38)
     if (c.pool) c.freeq.push_back(c.table.at(victim->second).phys);   // its block is free again
     c.table.erase(victim->second);
-    c.lru.erase(victim);
+    victim = c.lru.erase(victim);
     ++c.evictions;
   }
+}
+
+// Pinning (R38): can this request's eviction step find enough victims?  It needs size + new -
+// capacity of them among the UNPINNED entries it does not use itself (its served entries and its
+// new ones are the most recent and pinned by it after admission).  Checked before the request
+// mutates anything; a refused request is not admitted at all.
+bool pin_feasible(const Ctx& c, const std::vector<uint64_t>& served,
+                  const std::vector<uint64_t>& ins) {
+  if (!c.pin || !c.capacity) return true;
+  int64_t fresh = 0;
+  for (uint64_t k : ins) fresh += !present(c, k);
+  const int64_t need = (int64_t)c.table.size() + fresh - (int64_t)c.capacity;
+  if (need <= 0) return true;
+  std::unordered_map<uint64_t, int> own;
+  for (uint64_t k : served) own[k] = 1;
+  int64_t avail = 0;
+  for (auto& kv : c.table) avail += kv.second.pins == 0 && !own.count(kv.first);
+  return avail >= need;
 }
 
 }  // namespace
@@ -227,7 +255,48 @@ void* oracle_create(uint32_t block_size, uint64_t seed, int policy) {
   c->capacity = 0;
   c->evictions = 0;
   c->pool = 0;
+  c->pin = false;
+  c->admitted = 0;
   return c;
+}
+
+// In-flight pinning (R38).  Needs the block pool (physical block ids name what is released).
+int oracle_set_pin(void* h, int on) {
+  Ctx* c = (Ctx*)h;
+  if (!c->table.empty() || (on && !c->pool)) return 1;
+  c->pin = on != 0;
+  return 0;
+}
+
+// Release one pin on the entry holding each listed physical block (NONE entries skipped), e.g.
+// a finished request's block-table row.  1 if a block holds no live pinned entry (the other
+// blocks are still released).
+int oracle_release(void* h, const uint32_t* phys, uint64_t n) {
+  Ctx& c = *(Ctx*)h;
+  int err = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (phys[i] == (uint32_t)NONE) continue;
+    if (phys[i] >= c.key_of_phys.size()) { err = 1; continue; }
+    auto it = c.table.find(c.key_of_phys[phys[i]]);
+    if (it == c.table.end() || it->second.phys != phys[i] || it->second.pins == 0) { err = 1; continue; }
+    --it->second.pins;
+  }
+  return err;
+}
+
+uint64_t oracle_admitted(void* h) { return ((Ctx*)h)->admitted; }
+
+// Pin counts of the live entries, sorted by key (as oracle_dump).
+uint64_t oracle_dump_pins(void* h, uint64_t* keys, uint32_t* pins, uint64_t cap) {
+  Ctx& c = *(Ctx*)h;
+  std::vector<std::pair<uint64_t, uint32_t>> v;
+  for (auto& kv : c.table) v.push_back(std::make_pair(kv.first, kv.second.pins));
+  std::sort(v.begin(), v.end());
+  for (uint64_t i = 0; i < std::min<uint64_t>(cap, v.size()); ++i) {
+    keys[i] = v[i].first;
+    pins[i] = v[i].second;
+  }
+  return v.size();
 }
 
 // LRU capacity in entries (0 = unbounded).  Must be set on an empty table.
@@ -247,6 +316,7 @@ int oracle_set_pool(void* h, uint64_t pool) {
   c->pool = pool;
   c->freeq.clear();
   for (uint64_t i = 0; i < pool; ++i) c->freeq.push_back((uint32_t)i);
+  c->key_of_phys.assign(pool, 0);
   return 0;
 }
 
@@ -354,7 +424,9 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
   std::vector<uint64_t> hsh, hsh2, S, S2, Kk, I;
   const bool two = c.components == 2;
   if (c.pool) c.btab.assign(n_req ? (offsets[n_req] + c.bs - 1) / c.bs : 0, (uint32_t)NONE);
-  for (uint64_t j = 0; j < n_req; ++j, ++c.next_seq) {
+  c.admitted = 0;
+  std::vector<uint64_t> sv, iv;       // pinning check: the request's served / inserted keys
+  for (uint64_t j = 0; j < n_req; ++j, ++c.next_seq, c.admitted = j) {
     const uint32_t u = users[j];
     const bool e = enforce ? enforce[j] != 0 : true;
     const uint32_t* tok = tokens + offsets[j];
@@ -385,6 +457,11 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
         I[b] = two ? key2_of(T, T2) : key_of(T);
       }
       while (r < n && present(c, I[r + 1])) ++r;
+      if (c.pin) {
+        sv.assign(I.begin() + 1, I.begin() + 1 + r);
+        iv.assign(I.begin() + 1 + r, I.begin() + 1 + n);
+        if (!pin_feasible(c, sv, iv)) return 5;
+      }
       for (uint32_t b = 1; b <= r; ++b) touch(c, I[b], c.next_seq);
       for (uint32_t b = r + 1; b <= n; ++b) insert_if_absent(c, I[b], u, c.next_seq);
       f = 0;
@@ -410,6 +487,11 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
       if (c.policy == 0) {
         // Prefix Caching baseline: full reuse, new entries tagged with owner, no flags.
         r = k;
+        if (c.pin) {
+          sv.assign(Kk.begin() + 1, Kk.begin() + 1 + k);
+          iv.assign(Kk.begin() + 1 + k, Kk.begin() + 1 + n);
+          if (!pin_feasible(c, sv, iv)) return 5;
+        }
         for (uint32_t b = 1; b <= k; ++b) touch(c, Kk[b], c.next_seq);
         for (uint32_t b = k + 1; b <= n; ++b) insert_if_absent(c, Kk[b], u, c.next_seq);
       } else {
@@ -429,6 +511,11 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
           // "the Detector flags this prefix" — the last reused entry e_r (R2/D2).
           // Metadata is updated even when isolation is deactivated (R11).
           r = k;
+          if (c.pin) {
+            sv.assign(Kk.begin() + 1, Kk.begin() + 1 + k);
+            iv.assign(Kk.begin() + 1 + k, Kk.begin() + 1 + n);
+            if (!pin_feasible(c, sv, iv)) return 5;
+          }
           if (k >= 1 && owner_of(c, Kk[k]) != u && !flagged(c, Kk[k])) {
             c.table.at(Kk[k]).sharer = u;
             flagd = k;
@@ -460,6 +547,12 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
           uint32_t m = 0;
           while ((uint32_t)f + m < n && present(c, I[(uint32_t)f + m + 1])) ++m;
           r = (uint32_t)f + m;
+          if (c.pin) {
+            sv.assign(Kk.begin() + 1, Kk.begin() + 1 + f);
+            sv.insert(sv.end(), I.begin() + 1 + f, I.begin() + 1 + r);
+            iv.assign(I.begin() + 1 + r, I.begin() + 1 + n);
+            if (!pin_feasible(c, sv, iv)) return 5;
+          }
           // served: Shared K[1..f] (the flagged entry included; SPEC S:157 open question) and
           // Iso I[f+1..r].  Truncated Shared entries K[f+1..k] are not served (R23).
           for (uint32_t b = 1; b <= (uint32_t)f; ++b) touch(c, Kk[b], c.next_seq);
@@ -474,6 +567,7 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
       for (uint64_t key : c.fresh) {
         if (c.freeq.empty()) return 4;                       // pool exhausted (no eviction)
         c.table.at(key).phys = c.freeq.front();
+        c.key_of_phys[c.freeq.front()] = key;
         c.freeq.pop_front();
       }
       // R27: block table = the physical block of the entry holding each block's key as the
@@ -484,6 +578,7 @@ int oracle_process(void* h, uint64_t n_req, const uint32_t* tokens, const uint64
         const uint64_t key = (c.policy == 1 || (f >= 0 && (int64_t)b > (int64_t)f)) ? I[b] : Kk[b];
         auto it = c.table.find(key);
         c.btab[bt0 + b - 1] = it == c.table.end() ? (uint32_t)NONE : it->second.phys;
+        if (c.pin && it != c.table.end()) ++it->second.pins;   // R38: held until released
       }
     }
     oracle_result& o = out[j];
@@ -544,6 +639,8 @@ void oracle_copy_table(void* dst, void* src) {
   d->components = s->components;
   d->pool = s->pool;
   d->freeq = s->freeq;
+  d->pin = s->pin;
+  d->key_of_phys = s->key_of_phys;
 }
 
 void oracle_reserve(void* h, uint64_t n) { ((Ctx*)h)->table.reserve(n); }

@@ -31,7 +31,7 @@ ENTRY_EX_DTYPE = np.dtype([("key", "<u8"), ("owner", "<u4"), ("sharer", "<u4"),
 ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup_batch",
                "solid_insert_batch", "solid_admit_host", "solid_admit_host_u16", "solid_stats", "solid_dump", "solid_dump_ex",
                "solid_admit_batch", "solid_batch_status", "solid_block_keys", "solid_debug_set_epoch", "solid_debug_set_max_rounds",
-               "solid_block_table", "solid_dump_phys",
+               "solid_block_table", "solid_dump_phys", "solid_release", "solid_pins",
                "solid_reset", "solid_checkpoint", "solid_restore", "solid_last_error",
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
                "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit",
@@ -56,7 +56,7 @@ class _Config(ctypes.Structure):
                 ("policy", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("world", ctypes.c_uint32), ("rank", ctypes.c_uint32),
                 ("evict", ctypes.c_uint32), ("hash_components", ctypes.c_uint32),
-                ("block_table", ctypes.c_uint32)]
+                ("block_table", ctypes.c_uint32), ("pin", ctypes.c_uint32)]
 
 
 class _Batch(ctypes.Structure):
@@ -139,6 +139,10 @@ def load_library(path: str = LIB_PATH):
     lib.solid_dump_phys.restype = st
     lib.solid_dump_phys.argtypes = [vp, vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
     lib.solid_dump_ex.argtypes = [vp, vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+    lib.solid_release.restype = st
+    lib.solid_release.argtypes = [vp, vp, ctypes.c_uint64, vp]
+    lib.solid_pins.restype = st
+    lib.solid_pins.argtypes = [vp, vp]
     for name in ["solid_reset", "solid_checkpoint", "solid_restore"]:
         getattr(lib, name).restype = st
         getattr(lib, name).argtypes = [vp]
@@ -185,15 +189,18 @@ class Index:
                  max_batch_tokens: int = 1 << 24, max_batch_requests: int = 1 << 16,
                  max_blocks: int = 8192, seed: int = 0x5011D000, device: int = 0,
                  world: int = 1, rank: int = 0, evict: bool = False, hash_components: int = 1,
-                 block_table: bool = False):
+                 block_table: bool = False, pin: bool = False):
         """evict=True: LRU eviction at capacity_blocks instead of
         SOLID_ERR_CAPACITY; lookup() then synchronises its stream.  hash_components=2: H-def v3
         two-component keys.  block_table=True: physical KV block ids and
-        per-request block tables (admission synchronous)."""
+        per-request block tables (admission synchronous).  pin=True (with
+        block_table): in-flight pinning — each admitted request pins its row's entries until
+        release() (R38)."""
         self.lib = load_library()
         cfg = _Config(16, max_blocks, capacity_blocks, max_batch_tokens, max_batch_requests,
                       seed & 0xFFFFFFFFFFFFFFFF, POLICY[policy], device, world, rank,
-                      1 if evict else 0, hash_components, 1 if block_table else 0)
+                      1 if evict else 0, hash_components, 1 if block_table else 0,
+                      1 if pin else 0)
         self.world, self.rank = world, rank
         h = ctypes.c_void_p()
         rc = self.lib.solid_init(ctypes.byref(cfg), ctypes.byref(h))
@@ -397,6 +404,18 @@ class Index:
         self._check(self.lib.solid_dump_phys(self.h, ctypes.c_void_p(k.ctypes.data),
                                              ctypes.c_void_p(p.ctypes.data), m, ctypes.byref(n)))
         return k[:m], p[:m]
+
+    def release(self, phys, stream=None):
+        """solid_release: one pin less on the entry holding each physical block of `phys` (a
+        CUDA int32/uint32 tensor, e.g. a finished request's block-table row; -1 = NONE)."""
+        self._check(self.lib.solid_release(self.h, ctypes.c_void_p(phys.data_ptr()),
+                                           int(phys.numel()), self._stream(stream)))
+
+    def pins(self, n_blocks: int) -> np.ndarray:
+        """solid_pins: pin count per physical block (uint32 [capacity_blocks])."""
+        out = np.zeros(max(n_blocks, 1), dtype=np.uint32)
+        self._check(self.lib.solid_pins(self.h, ctypes.c_void_p(out.ctypes.data)))
+        return out[:n_blocks]
 
     def reset(self):
         self._check(self.lib.solid_reset(self.h))

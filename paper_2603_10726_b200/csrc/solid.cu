@@ -265,11 +265,12 @@ __device__ __forceinline__ bool init_id_at(const KParams& kp, uint32_t id, uint6
   if (kp.evict && present) {
     // eviction window: the entry's LRU rank among the live entries at batch start
     // (valid records before its own); only ranks below ebound can be evicted by this batch
+    // ranks count the EVICTABLE records only (pin mode: pinned entries are not in lbits, R38)
     const uint32_t p = kp.lpos[ipos];
     const uint32_t rank = kp.lpc[p >> 5] + __popc(kp.lbits[p >> 5] & ((1u << (p & 31)) - 1u));
     const unsigned long long tot = kp.ev_live0 + *kp.sum_blocks;
     const unsigned long long ebound = tot > kp.ev_cap ? tot - kp.ev_cap : 0ull;
-    if (rank < ebound) {
+    if (rank < ebound && ((kp.lbits[p >> 5] >> (p & 31)) & 1u)) {
       const uint32_t w = atomicAdd(kp.win_cnt, 1u);
       kp.win_id[w] = id;
       kp.win_rank[w] = rank;
@@ -1444,6 +1445,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
     return SOLID_ERR_INVALID;
   if (cfg->hash_components > 2) return SOLID_ERR_INVALID;
   if (cfg->block_table > 1 || (cfg->block_table && world != 1)) return SOLID_ERR_INVALID;
+  if (cfg->pin > 1 || (cfg->pin && !cfg->block_table)) return SOLID_ERR_INVALID;
   ctx = new solid_ctx();
   ctx->cfg = *cfg;
   ctx->cfg.world = world;

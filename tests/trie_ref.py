@@ -21,7 +21,7 @@ class TrieRef:
     value, needed only for the tie-break ("ties broken by smaller hash value")."""
 
     def __init__(self, block_size: int = 16, policy: int = 2, capacity: int = 0, keyfn=None,
-                 pool: int = 0):
+                 pool: int = 0, pin: bool = False):
         self.bs = block_size
         self.policy = policy
         self.table = {}     # name -> [owner, sharer]
@@ -39,6 +39,35 @@ class TrieRef:
         self.phys = {}                                       # name -> block
         self.events = 0
         self.fresh = []
+        # in-flight pinning (R38), brute force: every admitted request adds one pin to each entry
+        # of its row until released; eviction takes the min (last_used, key) over unpinned
+        # entries only; a request that would need more victims than there are unpinned entries
+        # it does not use itself is refused before anything changes
+        self.pin = pin
+        self.pins = {}                                       # name -> pin count
+
+    class Refused(Exception):
+        pass
+
+    def _check(self, served, inserts):
+        if not (self.pin and self.capacity):
+            return
+        new = [nm for nm in inserts if nm not in self.table]
+        need = len(self.table) + len(new) - self.capacity
+        own = set(served)
+        avail = sum(1 for nm in self.table if self.pins.get(nm, 0) == 0 and nm not in own)
+        if need > avail:
+            raise TrieRef.Refused()
+
+    def release(self, row):
+        """Drop one pin per physical block of a row (NONE skipped)."""
+        by_block = {b: nm for nm, b in self.phys.items() if nm in self.table}
+        for b in row:
+            if b == NONE:
+                continue
+            nm = by_block[b]
+            assert self.pins.get(nm, 0) > 0
+            self.pins[nm] -= 1
 
     def _served(self, names):
         for nm in names:
@@ -52,9 +81,11 @@ class TrieRef:
 
     def _evict(self):
         while self.capacity and len(self.table) > self.capacity:
-            victim = min(self.table, key=lambda nm: (self.last_used[nm], self.keyfn(nm)))
+            victim = min((nm for nm in self.table if self.pins.get(nm, 0) == 0),
+                         key=lambda nm: (self.last_used[nm], self.keyfn(nm)))
             del self.table[victim]
             del self.last_used[victim]
+            self.pins.pop(victim, None)
             self.evictions += 1
             if self.pool:
                 self.freed_at[self.phys.pop(victim)] = self.events
@@ -75,6 +106,7 @@ class TrieRef:
             names = [("I", (), u, tuple(blk[:b])) for b in range(1, n + 1)]
             while r < n and names[r] in t:
                 r += 1
+            self._check(names[:r], names[r:])
             self._served(names[:r])
             for b in range(r, n):
                 self._insert(t, names[b], u)
@@ -86,6 +118,7 @@ class TrieRef:
                 k += 1
             if self.policy == 0:
                 r = k
+                self._check(shared[:k], shared[k:])
                 self._served(shared[:k])
                 for b in range(k, n):
                     self._insert(t, shared[b], u)
@@ -100,6 +133,7 @@ class TrieRef:
                             break
                 if f < 0:
                     r = k
+                    self._check(shared[:k], shared[k:])
                     if k >= 1:
                         ent = t[shared[k - 1]]
                         if ent[0] != u and ent[1] == NONE:
@@ -116,6 +150,7 @@ class TrieRef:
                     while m < len(iso) and iso[m] in t:
                         m += 1
                     r = f + m
+                    self._check(shared[:f] + iso[:m], iso[m:])
                     self._served(shared[:f] + iso[:m])
                     for name in iso[m:]:
                         self._insert(t, name, u)
@@ -129,6 +164,10 @@ class TrieRef:
                 del self.freed_at[blk_id]
                 self.phys[name] = blk_id
             self.table_row = [self.phys.get(nm, NONE) if nm in t else NONE for nm in used]
+            if self.pin:
+                for nm in used:
+                    if nm in t:
+                        self.pins[nm] = self.pins.get(nm, 0) + 1
         self.clock += 1
         bits = ((1 if r > 0 else 0) | (2 if (n > 0 and r == n) else 0) | (4 if f >= 0 else 0)
                 | (8 if (f >= 0 and f < k) else 0) | (16 if flagd > 0 else 0))
