@@ -33,8 +33,9 @@ class Pair:
         """Admit b on the GPU; returns per request (result or None if refused, row)."""
         import torch
         P = self.P
+        d = P.to_device(b)           # the block table reads the batch's offsets: keep them alive
         try:
-            res = P.as_numpy(self.idx.admit(**P.to_device(b)))
+            res = P.as_numpy(self.idx.admit(**d))
         except P.SolidError as e:
             assert e.status == P.SOLID_ERR_CAPACITY, e
             if b.n_requests == 1:
