@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -310,9 +311,38 @@ __device__ bool init_id(const KParams& kp, uint32_t id, uint64_t key, uint64_t s
   return init_id_at(kp, id, key, present, owner, sharer, ipos);
 }
 
-// Warp-cooperative find-or-insert of one key per active lane.  Returns the key's id (0 only on
+// A tile of TW lanes (32: the warp; 16: half a warp) that works on one request.  Its collective
+// operations use the tile's own lane mask, so the two halves of a warp may take different paths
+// (each evaluates its own request).  ballot() returns the tile's bits in the low TW positions.
+template <int TW>
+struct Tile {
+  uint32_t mask;
+  int base;
+  __device__ __forceinline__ Tile() {
+    if (TW == 32) {
+      mask = 0xffffffffu;
+      base = 0;
+    } else {
+      base = (int)(threadIdx.x & 31) & ~(TW - 1);
+      mask = ((1u << TW) - 1u) << base;
+    }
+  }
+  __device__ __forceinline__ uint32_t ballot(bool p) const {
+    return TW == 32 ? __ballot_sync(0xffffffffu, p) : (__ballot_sync(mask, p) >> base);
+  }
+  template <class T>
+  __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, src, TW); }
+  template <class T>
+  __device__ __forceinline__ T shfl_up(T v, unsigned d) const {
+    return __shfl_up_sync(mask, v, d, TW);
+  }
+  __device__ __forceinline__ bool all(bool p) const { return __all_sync(mask, p); }
+};
+
+// Tile-cooperative (TW lanes) find-or-insert of one key per active lane.  Returns the key's id (0 only on
 // scratch overflow); `created` is set for the lane whose CAS published the key.  New ids are
 // allocated with one atomic per warp and probe step (segment `seg`).
+template <int TW = 32>
 __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool active, uint64_t key,
                                                      uint32_t seg, int lane, bool& created,
                                                      bool* snap_present = nullptr,
@@ -325,6 +355,7 @@ __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool act
   bool have_e = false;           // e holds the slot's current value from a failed CAS
   ulonglong2 e = make_ulonglong2(0, 0);
   created = false;
+  const Tile<TW> T;
   for (uint64_t probes = 0;; ++probes) {
     bool want = false;
     if (!done) {
@@ -341,11 +372,11 @@ __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool act
         want = true;                                // stale or never used: claim it
       }
     }
-    const uint32_t wm = __ballot_sync(0xffffffffu, want);
+    const uint32_t wm = T.ballot(want);
     if (wm) {
       uint32_t base = 0;
       if (lane == __ffs(wm) - 1) base = atomicAdd(&kp.seg_cnt[seg].v, (uint32_t)__popc(wm));
-      base = __shfl_sync(0xffffffffu, base, __ffs(wm) - 1);
+      base = T.shfl(base, __ffs(wm) - 1);
       if (want) {
         const uint32_t idx = base + __popc(wm & ((1u << lane) - 1u));
         if (idx >= kp.seg_cap) {
@@ -377,7 +408,7 @@ __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool act
         }
       }
     }
-    if (__all_sync(0xffffffffu, done)) break;
+    if (T.all(done)) break;
     if (probes > kp.smask) {
       if (!done) set_err(kp.st, ERR_SCRATCH);
       break;
@@ -697,10 +728,14 @@ __device__ __forceinline__ bool iso_visible(const KParams& kp, uint32_t id, int 
   return ldw64(&h->v[2 * R]) < limR || ldw64(&h->v[2 - 2 * R]) < limW;
 }
 
-// Evaluates request j in round t; returns true (warp-uniform) if its decision differs from the
-// previous round's (always true in round 1).
-template <int POLICY, bool DIST>
+// Evaluates request j in round t with a tile of TW lanes (lane = the lane within the tile);
+// returns true (tile-uniform) if its decision differs from the previous round's (always true in
+// round 1).  TW = 16: two requests per warp, each half walking 4 x 16 blocks per step — twice
+// the requests in flight per SM at the same register count (the rounds are latency-bound).
+template <int POLICY, bool DIST, int TW = 32>
 __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint64_t j, int lane) {
+  const Tile<TW> T;
+  constexpr uint32_t STEP = 4 * TW;          // blocks per walk step (4 groups in flight)
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
   const uint64_t o0 = kp.offsets[j], o1 = kp.offsets[j + 1];
   const uint32_t u = kp.users[j];
@@ -731,7 +766,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   // During round t, P[R] holds only the snapshot tag, round t-1's tag and older (numerically
   // larger) tags, so "visible to request seqp" is one 64-bit compare v < limR = tagR<<32 | seqp
   // (snapshot values carry the smallest tag and always pass); likewise "flagged".  Blocks are
-  // walked 128 at a time: ids and P[R] pairs of 4 groups of 32 are in flight together.
+  // walked STEP at a time: ids and P[R] pairs of 4 groups of TW are in flight together.
   const unsigned long long limR = ((unsigned long long)tagR << 32) | seqp;
   const unsigned long long limW = DIST ? 0ull : ((unsigned long long)tagW << 32) | seqp;
   uint32_t k = n;
@@ -739,39 +774,39 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   bool carry_flag = false;    // flagged(index g-1) from the previous group
   bool walked = false;
   bool iso_pre_vis = false;
-  uint32_t idq[4];            // ids of the last walked 128 blocks (from wbase), kept for the scatter
+  uint32_t idq[4];            // ids of the last walked STEP blocks (from wbase), kept for the scatter
   uint32_t wbase = 0;
-  for (uint32_t base = 0; base <= n && !walked; base += 128) {
+  for (uint32_t base = 0; base <= n && !walked; base += STEP) {
     wbase = base;
     ulonglong2 pq[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint32_t i = base + 32 * q + lane;
+      const uint32_t i = base + TW * q + lane;
       idq[q] = i < n ? sh_ids[i] : 0u;
     }
     if (POLICY == SOLID_POLICY_SOLIDARITY && base == 0 && fprev >= 1 && (uint32_t)fprev + lane < n)
       iso_pre_vis = iso_visible(kp, iso_pre_id, R, limR, limW);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint32_t i = base + 32 * q + lane;
+      const uint32_t i = base + TW * q + lane;
       pq[q] = make_ulonglong2(~0ull, ~0ull);
       if (i < n) pq[q] = ldw128(&kp.hot[idq[q]].v[2 * R]);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint32_t g = base + 32 * q;
+      const uint32_t g = base + TW * q;
       if (g > n) break;
       const bool vis = pq[q].x < limR;                  // invalid lanes hold ~0: not visible
       const bool fl = POLICY == SOLID_POLICY_SOLIDARITY && pq[q].y < limR;
-      const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
-      const int L = inv ? __ffs(inv) - 1 : 32;          // first invisible lane in this group
+      const uint32_t inv = T.ballot(!vis);
+      const int L = inv ? __ffs(inv) - 1 : TW;          // first invisible lane in this group
       if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
         // lane evaluates the barrier condition for index m = i - 1 (needs flagged(m) and the
         // owner of the NEXT entry i): stop at m iff flagged(m) and not (i visible and
         // owned by the requester).  Groups without flagged entries skip it (the common case).
-        const uint32_t flm = __ballot_sync(0xffffffffu, fl);
+        const uint32_t flm = T.ballot(fl);
         if (flm || carry_flag) {
-          bool pf = __shfl_up_sync(0xffffffffu, fl, 1);
+          bool pf = T.shfl_up(fl, 1);
           if (lane == 0) pf = carry_flag;
           bool cond = false;
           if (pf && lane <= L && !(g == 0 && lane == 0)) {
@@ -781,12 +816,12 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
                 vis && (DIST ? kp.mown[idq[q]] : owner_from(kp, idq[q], first)) == u;
             cond = !pass;
           }
-          const uint32_t cm = __ballot_sync(0xffffffffu, cond);
+          const uint32_t cm = T.ballot(cond);
           if (cm) f = (int32_t)(g + (uint32_t)(__ffs(cm) - 1));   // 1-based depth = m + 1 = i
         }
-        carry_flag = (flm >> 31) & 1u;
+        carry_flag = (flm >> (TW - 1)) & 1u;
       }
-      if (L < 32) {
+      if (L < TW) {
         k = g + (uint32_t)L;
         walked = true;
         break;
@@ -805,12 +840,12 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
       // carries their index snapshot); the first group was prefetched above
       // kIsoG groups with their id and state loads in flight together (long isolated walks)
       bool stop = false;
-      for (uint32_t g0 = (uint32_t)f; g0 < n && !stop; g0 += 32 * kIsoG) {
+      for (uint32_t g0 = (uint32_t)f; g0 < n && !stop; g0 += TW * kIsoG) {
         uint32_t idv[kIsoG];
         unsigned long long va[kIsoG], vb[kIsoG];
 #pragma unroll
         for (int q = 0; q < kIsoG; ++q) {
-          const uint32_t i = g0 + 32 * q + lane;
+          const uint32_t i = g0 + TW * q + lane;
           idv[q] = (i < n && !(q == 0 && g0 == (uint32_t)f)) ? iso_ids[i] : 0u;
         }
 #pragma unroll
@@ -824,12 +859,12 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
         }
 #pragma unroll
         for (int q = 0; q < kIsoG; ++q) {
-          const uint32_t g = g0 + 32 * q;
+          const uint32_t g = g0 + TW * q;
           if (g >= n) break;
           const uint32_t i = g + lane;
           const bool vis = (q == 0 && g0 == (uint32_t)f) ? (i < n && iso_pre_vis)
                                                           : (idv[q] && (va[q] < limR || vb[q] < limW));
-          const uint32_t inv = __ballot_sync(0xffffffffu, !vis);
+          const uint32_t inv = T.ballot(!vis);
           if (inv) {
             m = g + (uint32_t)(__ffs(inv) - 1) - (uint32_t)f;
             stop = true;
@@ -846,13 +881,13 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
       const uint64_t sig2 = kp.nc == 2 ? sigma2_of(kp.seed, u) : 0;
       const uint64_t gf2 = kp.nc == 2 ? kp.gtab2[f] : 0;
       bool found = false;
-      for (uint32_t g = (uint32_t)f; g < n; g += 32) {
+      for (uint32_t g = (uint32_t)f; g < n; g += TW) {
         const uint32_t i = g + lane;
         const bool valid = i < n;
         uint64_t key = 0;
         if (valid) key = iso_key(kp, blk0 + i, i, sig, gf, sig2, gf2);
         bool created, snap = false;
-        const uint32_t id = scratch_register(kp, valid, key, seg, lane, created, &snap);
+        const uint32_t id = scratch_register<TW>(kp, valid, key, seg, lane, created, &snap);
         bool bvis = false;
         if (valid) {
           iso_ids[i] = id;
@@ -860,7 +895,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
         }
         // lanes not visible through the staged state may still be in the index snapshot; probe
         // them in order, only until the first key that is absent (the walk stops there)
-        uint32_t cand = __ballot_sync(0xffffffffu, valid && !bvis);
+        uint32_t cand = T.ballot(valid && !bvis);
         while (!found && cand) {
           const int L = __ffs(cand) - 1;
           bool present = false;
@@ -873,7 +908,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
               present = index_find(kp, key, ow, sr, ip);
             }
           }
-          present = __shfl_sync(0xffffffffu, present, L);
+          present = T.shfl(present, L);
           if (present) {
             cand &= cand - 1;
           } else {
@@ -904,7 +939,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
                          ((unsigned long long)tagW << 32) | (unsigned long long)seqp);
       }
     }
-    flagd = __shfl_sync(0xffffffffu, flagd, 0);
+    flagd = T.shfl(flagd, 0);
   }
 
   // ---- staged inserts (seq-min scatter); APC / USER_ISOLATION are exact from round 0 ----
@@ -915,27 +950,27 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
     // only inserts keys invisible to it), unlike the hot keys of K_A
     if (DIST) {
       const unsigned long long pk = ((unsigned long long)seqp << 32) | (unsigned long long)u;
-      for (uint32_t i = r + lane; i < n; i += 32) atomicMin(&kp.int_ins[ids[i]], pk);
+      for (uint32_t i = r + lane; i < n; i += TW) atomicMin(&kp.int_ins[ids[i]], pk);
     } else {
       // ids already in registers need no dependent load: a request diverting at an unchanged
-      // depth has blocks f..f+31 in iso_pre_id (lane l = block f + l); a Shared one has the
-      // last walked 128 blocks in idq (lane l of idq[q] = block wbase + 32 q + l)
+      // depth has blocks f..f+TW-1 in iso_pre_id (lane l = block f + l); a Shared one has the
+      // last walked STEP blocks in idq (lane l of idq[q] = block wbase + TW q + l)
       const bool pre = POLICY == SOLID_POLICY_SOLIDARITY && f >= 1 && f == fprev;
       const bool shr = f < 0;
-      for (uint32_t i0 = r; i0 < n; i0 += 32) {
+      for (uint32_t i0 = r; i0 < n; i0 += TW) {
         const uint32_t i = i0 + lane;
         uint32_t id = 0;
-        if (pre && i0 < (uint32_t)f + 32) {
-          const uint32_t v = __shfl_sync(0xffffffffu, iso_pre_id, (i - (uint32_t)f) & 31);
-          if (i < n) id = i < (uint32_t)f + 32 ? v : ids[i];
-        } else if (shr && i0 >= wbase && i0 < wbase + 128) {
-          const uint32_t src = (i - wbase) & 31, q = (i - wbase) >> 5;
-          const uint32_t v0 = __shfl_sync(0xffffffffu, idq[0], src);
-          const uint32_t v1 = __shfl_sync(0xffffffffu, idq[1], src);
-          const uint32_t v2 = __shfl_sync(0xffffffffu, idq[2], src);
-          const uint32_t v3 = __shfl_sync(0xffffffffu, idq[3], src);
+        if (pre && i0 < (uint32_t)f + TW) {
+          const uint32_t v = T.shfl(iso_pre_id, (int)((i - (uint32_t)f) & (TW - 1)));
+          if (i < n) id = i < (uint32_t)f + TW ? v : ids[i];
+        } else if (shr && i0 >= wbase && i0 < wbase + STEP) {
+          const uint32_t src = (i - wbase) & (TW - 1), q = (i - wbase) / TW;
+          const uint32_t v0 = T.shfl(idq[0], (int)src);
+          const uint32_t v1 = T.shfl(idq[1], (int)src);
+          const uint32_t v2 = T.shfl(idq[2], (int)src);
+          const uint32_t v3 = T.shfl(idq[3], (int)src);
           const uint32_t v = q == 0 ? v0 : q == 1 ? v1 : q == 2 ? v2 : v3;
-          if (i < n) id = i < wbase + 128 ? v : ids[i];
+          if (i < n) id = i < wbase + STEP ? v : ids[i];
         } else if (i < n) {
           id = ids[i];
         }
@@ -976,35 +1011,29 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   return changed;
 }
 
-// The resolver: all rounds in one persistent cooperative launch (grid = resident CTAs).  Warps
-// stride over the requests; between rounds a grid-wide barrier (which also invalidates L1, so the
-// next round sees every atomic of this one).  Stops at the first round
+// The resolver: all rounds in one persistent cooperative launch (grid = resident CTAs).  Tiles
+// of TW lanes stride over the requests; between rounds a grid-wide barrier (which also
+// invalidates L1, so the next round sees every atomic of this one).  Stops at the first round
 // t >= 2 whose decisions all equal round t-1's, or after t_max.
-template <int POLICY>
-__global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) {
+template <int POLICY, int TW>
+__device__ __forceinline__ void resolve_rounds(const KParams& kp, uint32_t t_max,
+                                               uint32_t* s_changed) {
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
-  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  if (grid.thread_rank() == 0) kp.st->round_ns[0] = globaltimer_ns();
-  if (blockIdx.x == 0 && threadIdx.x < 32) {     // K_A's distinct keys (its index probes)
-    unsigned long long c = 0;
-#pragma unroll
-    for (int q = 0; q < kNSeg / 32; ++q) c += min(kp.seg_cnt[lane + 32 * q].v, kp.seg_cap);
-    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) kp.st->ids_after_hash = c;
-  }
-  __shared__ uint32_t s_changed;
+  const int tl = lane & (TW - 1);                 // lane within the request's tile
+  constexpr int LOG = TW == 32 ? 5 : 4;
+  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> LOG;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> LOG;
   for (uint32_t t = 1; t <= t_max; ++t) {
-    if (threadIdx.x == 0) s_changed = 0;
+    if (threadIdx.x == 0) *s_changed = 0;
     __syncthreads();
     bool any = false;
     for (uint64_t j = kp.j_lo + w0; j < kp.n; j += nw)
-      any |= eval_request<POLICY, false>(kp, t, j, lane);
+      any |= eval_request<POLICY, false, TW>(kp, t, j, tl);
     // one store per CTA (100k same-address stores would serialise on one L2 slice)
-    if (lane == 0 && any) s_changed = 1;
+    if (tl == 0 && any) *s_changed = 1;
     __syncthreads();
-    if (threadIdx.x == 0 && s_changed) kp.st->changed[t] = kp.epoch;
+    if (threadIdx.x == 0 && *s_changed) kp.st->changed[t] = kp.epoch;
     if (POLICY != SOLID_POLICY_SOLIDARITY) {         // exact in one pass
       if (grid.thread_rank() == 0) kp.st->conv = 1;
       return;
@@ -1026,6 +1055,31 @@ __global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max) 
       return;
     }
   }
+}
+
+// Tile width per batch, decided on the device (the host does not know the batch's tokens in the
+// asynchronous paths): short requests (<= 64 blocks on average, e.g. C4) are resolved two per
+// warp (TW = 16: twice the requests in flight at the same registers, -23 % on C4), long ones a
+// warp each (a 16-lane tile needs twice the dependent walk steps: +20 % on C2 / C3).
+template <int POLICY>
+__global__ void __launch_bounds__(256, 4) k_resolve(KParams kp, uint32_t t_max, int tile) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) kp.st->round_ns[0] = globaltimer_ns();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {     // K_A's distinct keys (its index probes)
+    const int lane = threadIdx.x;
+    unsigned long long c = 0;
+#pragma unroll
+    for (int q = 0; q < kNSeg / 32; ++q) c += min(kp.seg_cnt[lane + 32 * q].v, kp.seg_cap);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) kp.st->ids_after_hash = c;
+  }
+  __shared__ uint32_t s_changed;
+  bool half = tile == 16;
+  if (tile == 0) {                                // auto: average full blocks per request
+    const uint64_t T = kp.offsets[kp.n] - kp.offsets[kp.j_lo];
+    half = T <= (uint64_t)64 * 16 * (kp.n - kp.j_lo);
+  }
+  if (half) resolve_rounds<POLICY, 16>(kp, t_max, &s_changed);
+  else resolve_rounds<POLICY, 32>(kp, t_max, &s_changed);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1286,6 +1340,7 @@ struct solid_ctx {
   uint32_t tf = 0;
   uint32_t rounds = 0;
   uint32_t max_rounds = kMaxRounds;      // resolver round limit (solid_debug_set_max_rounds)
+  int resolve_tw = 0;                    // resolver lanes per request: 0 auto (SOLID_RESOLVE_TILE)
   bool split_last = false;               // the last batch was committed in parts (non-convergence)
   cudaStream_t stream = nullptr;
   // host-buffer admission staging
@@ -1450,6 +1505,10 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   ctx->cfg = *cfg;
   ctx->cfg.world = world;
   ctx->dev = cfg->device;
+  if (const char* e = getenv("SOLID_RESOLVE_TILE")) {
+    const int v = atoi(e);
+    ctx->resolve_tw = (v == 16 || v == 32) ? v : 0;
+  }
   CK(cudaSetDevice(ctx->dev));
   // evict mode: 4x headroom so the tombstones of ~C/4 evictions fit between rebuilds
   ctx->tcap = next_pow2(std::max<uint64_t>((cfg->evict ? 4 : 2) * cfg->capacity_blocks, 1024));
@@ -1602,7 +1661,8 @@ static solid_status launch_resolve(solid_ctx* ctx, cudaStream_t s) {
   const uint64_t need = ((ctx->kp.n - ctx->kp.j_lo) * 32 + 255) / 256;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ctx->resolve_ctas, need));
   uint32_t tmax = ctx->max_rounds;
-  void* args[] = {(void*)&ctx->kp, (void*)&tmax};
+  int tile = ctx->resolve_tw;
+  void* args[] = {(void*)&ctx->kp, (void*)&tmax, (void*)&tile};
   CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, s));
   return SOLID_OK;
 }
