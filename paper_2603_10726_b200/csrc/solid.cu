@@ -134,6 +134,7 @@ struct KParams {
   unsigned long long* int_ins;     // per local id: this round's earliest local inserter (seq'<<32|user)
   unsigned long long* int_flg;     // per local id: this round's earliest local flagger
   uint32_t* mown;                  // per local id: owner user of the mirrored first inserter
+  ulonglong2* lint;                // per local id: the intents last sent to its owner (delta INT)
   uint32_t* long_q;                // K_A: requests longer than kLongBlocks (CTA path)
   uint32_t* pool_cnt;              // block_table: k_commit counts each request's new entries
   // LRU eviction mode (solid_evict.inc): keys of the batch whose LRU record lies
@@ -324,7 +325,7 @@ struct Tile {
       base = 0;
     } else {
       base = (int)(threadIdx.x & 31) & ~(TW - 1);
-      mask = ((1u << TW) - 1u) << base;
+      mask = ((1u << (TW & 31)) - 1u) << base;
     }
   }
   __device__ __forceinline__ uint32_t ballot(bool p) const {
@@ -390,6 +391,7 @@ __device__ __forceinline__ uint32_t scratch_register(const KParams& kp, bool act
             kp.int_ins[mine] = ~0ull;
             kp.int_flg[mine] = ~0ull;
             kp.mown[mine] = kNone;
+            kp.lint[mine] = make_ulonglong2(~0ull, ~0ull);
             __threadfence();  // visible before the CAS publishes the id
           }
           const ulonglong2 nv =
