@@ -486,6 +486,7 @@ def measure_configs(dev, args):
         r = P.as_numpy(o)
         out[name] = {"workload": desc, "ms_per_batch": med, "requests_per_s": s.n_requests / (med / 1e3),
                      "blocks_per_s": s.n_blocks() / (med / 1e3), "resolver_rounds": rounds[-1],
+                     "resolver_round_us": [round(x, 1) for x in st["round_us"]],
                      "phases_ms": {"hash": st["ms_hash"], "resolve": st["ms_resolve"],
                                    "commit": st["ms_commit"]},
                      "algorithmic_bytes": st["algorithmic_bytes"],

@@ -48,6 +48,7 @@ constexpr uint32_t kLongBlocks = 128;   // K_A: longer requests are hashed by a 
 constexpr uint64_t kLongMaxBatch = 148 * 32;   // ... in batches of at most this many requests
 constexpr int kIsoG = 4;                         // resolver: isolated-walk groups in flight
 constexpr uint32_t kMaxRounds = 4093;
+constexpr uint32_t kStampWaitNs = 12000;    // resolver main pass: longest wait for a stamp
 constexpr uint32_t kMaxEpoch = (0xFFFFFFFFu / 4096u) - 1;
 
 enum : uint32_t {
@@ -82,7 +83,7 @@ struct DevStatus {
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t seg[kNSeg];                   // id counts per segment (gathered by k_stats)
 #ifdef SOLID_COUNTERS
-  unsigned long long cnt[16][8];         // profiling build only: per-round path counters
+  unsigned long long cnt[16][12];        // profiling build only: per-round path counters
 #endif
   // last: round t's "some decision changed" holds the batch epoch (never reset; a stale value
   // can only cost one certifying round), so a batch clears and copies only the head above
@@ -123,6 +124,12 @@ struct KParams {
   uint32_t* iso_id;                // per block: id of its isolated key (valid for dec.f)
   uint64_t slot_cap;
   uint4* dec;
+  int stamp;                       // inserter-stamp rule on (SOLID_STAMP=0 turns it off for A/B)
+  uint32_t stamp_wait_ns;          // its wait bound in the main pass (kStampWaitNs)
+  uint32_t* dlist;                 // requests deferred by the main pass of a round (stale stamp)
+  uint32_t* dcnt;                  // [2]: their count, by round parity
+  unsigned long long* fst;         // per request: tag(round) << 32 | divert depth f of its latest
+                                   // evaluation (single GPU; read by later requests)
   solid_result* out;
   SegCounter* seg_cnt;
   uint32_t seg_cap;
@@ -185,6 +192,15 @@ __device__ __forceinline__ unsigned long long ldw64(const void* p) {
   unsigned long long r;
   asm volatile("ld.global.u64 %0, [%1];" : "=l"(r) : "l"(p));
   return r;
+}
+// Single-copy-atomic 64-bit accesses at gpu scope (the per-request round stamps, fst[]).
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long r;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // 128-bit compare-and-swap (ATOMG.E.CAS.128 on sm_90+).
@@ -734,8 +750,9 @@ __device__ __forceinline__ bool iso_visible(const KParams& kp, uint32_t id, int 
 // returns true (tile-uniform) if its decision differs from the previous round's (always true in
 // round 1).  TW = 16: two requests per warp, each half walking 4 x 16 blocks per step — twice
 // the requests in flight per SM at the same register count (the rounds are latency-bound).
-template <int POLICY, bool DIST, int TW = 32>
-__device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint64_t j, int lane) {
+template <int POLICY, bool DIST, int TW = 32, bool DEFER = false>
+__device__ __forceinline__ int eval_request(const KParams& kp, uint32_t t, uint64_t j, int lane) {
+  constexpr bool may_defer = DEFER;
   const Tile<TW> T;
   constexpr uint32_t STEP = 4 * TW;          // blocks per walk step (4 groups in flight)
   const uint32_t seg = (uint32_t)(j & (kNSeg - 1));
@@ -744,12 +761,12 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   const bool enf = (POLICY == SOLID_POLICY_SOLIDARITY) && (kp.enforce ? kp.enforce[j] != 0 : true);
   const uint4 prev =
       (POLICY == SOLID_POLICY_SOLIDARITY && t >= 2) ? kp.dec[j] : make_uint4(0, ~0u, 0, 0);
-  if (o1 < o0) return false;
+  if (o1 < o0) return 0;
   const uint64_t nb = (o1 - o0) >> 4;
-  if (nb > kp.max_blocks) return false;
+  if (nb > kp.max_blocks) return 0;
   const uint32_t n = (uint32_t)nb;
   const uint64_t blk0 = o0 >> 4;
-  if (n && blk0 + n > kp.slot_cap) return false;
+  if (n && blk0 + n > kp.slot_cap) return 0;
   const uint32_t* sh_ids = kp.id_of_block + blk0;       // this request's blocks (32-bit indexing)
   uint32_t* iso_ids = kp.iso_id + blk0;
   const uint32_t seqp = (uint32_t)(kp.seq_base + j + 1);
@@ -800,8 +817,8 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
       if (g > n) break;
       const bool vis = pq[q].x < limR;                  // invalid lanes hold ~0: not visible
       const bool fl = POLICY == SOLID_POLICY_SOLIDARITY && pq[q].y < limR;
-      const uint32_t inv = T.ballot(!vis);
-      const int L = inv ? __ffs(inv) - 1 : TW;          // first invisible lane in this group
+        const uint32_t inv = T.ballot(!vis);
+      int L = inv ? __ffs(inv) - 1 : TW;          // first invisible lane in this group
       if (POLICY == SOLID_POLICY_SOLIDARITY && enf && f < 0) {
         // lane evaluates the barrier condition for index m = i - 1 (needs flagged(m) and the
         // owner of the NEXT entry i): stop at m iff flagged(m) and not (i visible and
@@ -810,16 +827,63 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
         if (flm || carry_flag) {
           bool pf = T.shfl_up(fl, 1);
           if (lane == 0) pf = carry_flag;
-          bool cond = false;
+          bool cond = false, gone = false, stale = false;
           if (pf && lane <= L && !(g == 0 && lane == 0)) {
             const uint32_t first =
                 ((uint32_t)(pq[q].x >> 32) == tagS) ? 0u : (uint32_t)pq[q].x;
-            const bool pass =
-                vis && (DIST ? kp.mown[idq[q]] : owner_from(kp, idq[q], first)) == u;
+            bool pass = vis && (DIST ? kp.mown[idq[q]] : owner_from(kp, idq[q], first)) == u;
+            if (!DIST && pass && first != 0u && kp.stamp) {
+              // Inserter stamp: entry i passes the barrier because round t-1
+              // says an earlier request of this user inserted it.  If that request has already
+              // been evaluated in THIS round and now diverts at a depth <= i, it no longer
+              // inserts the Shared key: take the entry as absent (stop here, divert at m).  A
+              // guess like any Gauss-Seidel value; a request evaluated earlier in this round is
+              // waited for (it is < j, so the wait chain ends).  Sound for certification: in a
+              // round without changes the rule cannot fire (round t-1's inserter would not
+              // have inserted the key either).
+              const uint64_t ir = (uint64_t)first - 1u - kp.seq_base;
+              if (ir >= kp.j_lo && ir < j) {
+                unsigned long long v = ld_relaxed64(&kp.fst[ir]);
+                if (may_defer && (uint32_t)(v >> 32) != tagW) {
+                  // main pass (long requests): a short bounded wait (the inserter is being
+                  // evaluated right now, typically in the round's first wave), then defer the
+                  // request to the round's second pass, after a grid barrier.  Unbounded waits
+                  // would chain (each request depending on the previous one) and serialise the
+                  // round.  Short requests (two per warp) and the deferred pass never wait:
+                  // a stale stamp is simply no information (the Jacobi value is used).
+                  const unsigned long long t0 = globaltimer_ns();
+                  while ((uint32_t)(v >> 32) != tagW && globaltimer_ns() - t0 < kp.stamp_wait_ns) {
+                    __nanosleep(64);
+                    v = ld_relaxed64(&kp.fst[ir]);
+                  }
+                  stale = (uint32_t)(v >> 32) != tagW;
+                }
+                const int32_t fi = (int32_t)(uint32_t)v;
+                if ((uint32_t)(v >> 32) == tagW && fi >= 1 && (uint32_t)fi <= g + (uint32_t)lane) {
+                  pass = false;
+                  gone = true;
+                }
+#ifdef SOLID_COUNTERS
+                if (t < 16) {
+                  atomicAdd(&kp.st->cnt[t][8], gone ? 1ull : 0ull);
+                  atomicAdd(&kp.st->cnt[t][9], 1ull);
+
+                }
+#endif
+              }
+            }
             cond = !pass;
           }
           const uint32_t cm = T.ballot(cond);
           if (cm) f = (int32_t)(g + (uint32_t)(__ffs(cm) - 1));   // 1-based depth = m + 1 = i
+          if (!DIST) {
+            if (T.ballot(stale)) {                     // nothing written yet: evaluate it later
+              if (lane == 0) kp.dlist[atomicAdd(&kp.dcnt[t & 1], 1u)] = (uint32_t)j;
+              return 2;
+            }
+            const uint32_t gm = T.ballot(gone);
+            if (gm) L = min(L, __ffs(gm) - 1);         // the entry taken as absent ends the walk
+          }
         }
         carry_flag = (flm >> (TW - 1)) & 1u;
       }
@@ -984,6 +1048,8 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
   const uint4 d = make_uint4(k, (uint32_t)f, r, flagd);
   const bool changed =
       t == 1 || prev.x != d.x || prev.y != d.y || prev.z != d.z || prev.w != d.w;
+  if (!DIST && POLICY == SOLID_POLICY_SOLIDARITY && lane == 0)   // this round's stamp (every round)
+    st_relaxed64(&kp.fst[j], ((unsigned long long)tagW << 32) | (uint32_t)f);
 #ifdef SOLID_COUNTERS
   if (lane == 0 && t < 16) {
     unsigned long long* c = kp.st->cnt[t];
@@ -1010,7 +1076,7 @@ __device__ __forceinline__ bool eval_request(const KParams& kp, uint32_t t, uint
                ((f >= 0 && (uint32_t)f < kk) ? 8u : 0u) | (flagd > 0 ? 16u : 0u);
     kp.out[j] = res;
   }
-  return changed;
+  return changed ? 1 : 0;
 }
 
 // The resolver: all rounds in one persistent cooperative launch (grid = resident CTAs).  Tiles
@@ -1030,8 +1096,31 @@ __device__ __forceinline__ void resolve_rounds(const KParams& kp, uint32_t t_max
     if (threadIdx.x == 0) *s_changed = 0;
     __syncthreads();
     bool any = false;
-    for (uint64_t j = kp.j_lo + w0; j < kp.n; j += nw)
-      any |= eval_request<POLICY, false, TW>(kp, t, j, tl);
+    // (long requests only: with two short requests per warp, C4, moving every new divert into
+    // one round measured slower than the Jacobi order — 3.25 vs 2.18 ms for rounds 2 + 3)
+    const bool stamps = POLICY == SOLID_POLICY_SOLIDARITY && kp.stamp && TW == 32;
+    // main pass: every request; with the stamp rule, a deferred pass follows for the requests
+    // whose inserter stamp was stale in the main pass, after a grid barrier,
+    // when every main-pass stamp is published
+    if (stamps) {
+      for (uint64_t j = kp.j_lo + w0; j < kp.n; j += nw)
+        any |= eval_request<POLICY, false, TW, true>(kp, t, j, tl) == 1;
+      grid.sync();
+      const uint32_t nd = *(volatile uint32_t*)&kp.dcnt[t & 1];
+      if (grid.thread_rank() == 0) kp.dcnt[(t + 1) & 1] = 0;   // next round's list
+#ifdef SOLID_COUNTERS
+      const unsigned long long td0 = globaltimer_ns();
+#endif
+      for (uint64_t q = w0; q < nd; q += nw)
+        any |= eval_request<POLICY, false, TW, false>(kp, t, kp.dlist[q], tl) == 1;
+#ifdef SOLID_COUNTERS
+      if (tl == 0 && t < 16) atomicMax(&kp.st->cnt[t][10], globaltimer_ns() - td0);
+      if (grid.thread_rank() == 0 && t < 16) kp.st->cnt[t][11] = nd;
+#endif
+    } else {
+      for (uint64_t j = kp.j_lo + w0; j < kp.n; j += nw)
+        any |= eval_request<POLICY, false, TW, false>(kp, t, j, tl) == 1;
+    }
     // one store per CTA (100k same-address stores would serialise on one L2 slice)
     if (tl == 0 && any) *s_changed = 1;
     __syncthreads();
@@ -1321,6 +1410,11 @@ struct solid_ctx {
   uint32_t* iso_id = nullptr;
   uint64_t slot_cap = 0;
   uint4* dec = nullptr;
+  unsigned long long* fst = nullptr;
+  int stamp_rule = 1;
+  uint32_t stamp_wait_ns = kStampWaitNs;
+  uint32_t* dlist = nullptr;
+  uint32_t* dcnt = nullptr;
   SegCounter* seg_cnt = nullptr;
   uint32_t seg_cap = 0;
   DevStatus* st = nullptr;
@@ -1442,6 +1536,9 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->id_of_block);
   cudaFree(c->iso_id);
   cudaFree(c->dec);
+  cudaFree(c->fst);
+  cudaFree(c->dlist);
+  cudaFree(c->dcnt);
   cudaFree(c->seg_cnt);
   cudaFree(c->st);
   cudaFree(c->live_dev);
@@ -1507,6 +1604,8 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   ctx->cfg = *cfg;
   ctx->cfg.world = world;
   ctx->dev = cfg->device;
+  if (const char* e = getenv("SOLID_STAMP")) ctx->stamp_rule = atoi(e) != 0;
+  if (const char* e = getenv("SOLID_STAMP_WAIT")) ctx->stamp_wait_ns = (uint32_t)atoi(e);
   if (const char* e = getenv("SOLID_RESOLVE_TILE")) {
     const int v = atoi(e);
     ctx->resolve_tw = (v == 16 || v == 32) ? v : 0;
@@ -1538,6 +1637,9 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
             alloc((void**)&ctx->id_of_block, ctx->slot_cap * sizeof(uint32_t)) &&
             alloc((void**)&ctx->iso_id, ctx->slot_cap * sizeof(uint32_t)) &&
             alloc((void**)&ctx->dec, cfg->max_batch_requests * sizeof(uint4)) &&
+            alloc((void**)&ctx->fst, std::max<uint64_t>(cfg->max_batch_requests, 1) * sizeof(unsigned long long)) &&
+            alloc((void**)&ctx->dlist, std::max<uint64_t>(cfg->max_batch_requests, 1) * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->dcnt, 2 * sizeof(uint32_t)) &&
             alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(SegCounter)) &&
             alloc((void**)&ctx->st, sizeof(DevStatus)) &&
             alloc((void**)&ctx->live_dev, sizeof(unsigned long long)) &&
@@ -1740,6 +1842,11 @@ static solid_status lookup_setup(solid_ctx* ctx, const solid_batch* b, solid_res
   kp.iso_id = ctx->iso_id;
   kp.slot_cap = ctx->slot_cap;
   kp.dec = ctx->dec;
+  kp.fst = ctx->fst;
+  kp.stamp = ctx->stamp_rule;
+  kp.stamp_wait_ns = ctx->stamp_wait_ns;
+  kp.dlist = ctx->dlist;
+  kp.dcnt = ctx->dcnt;
   kp.out = out;
   // the CTA-per-request path pays only when the batch has fewer requests than the GPU has
   // resident warps (148 SMs x 32): with more, warp-per-request already fills the machine and
@@ -1751,6 +1858,7 @@ static solid_status lookup_setup(solid_ctx* ctx, const solid_batch* b, solid_res
   kp.st = ctx->st;
   CK(cudaMemsetAsync(ctx->st, 0, kStHead, s));
   CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
+  CK(cudaMemsetAsync(ctx->dcnt, 0, 2 * sizeof(uint32_t), s));
   // the block table describes the last COMMITTED batch; this lookup replaces the batch arrays it
   // is built from, so it is unavailable until this batch commits
   pool_invalidate(ctx);
@@ -1940,6 +2048,7 @@ static solid_status admit_range(solid_ctx* ctx, uint64_t lo, uint64_t hi, cudaSt
   kp.n = hi;
   CK(cudaMemsetAsync(ctx->st, 0, kStHead, s));
   CK(cudaMemsetAsync(ctx->seg_cnt, 0, kNSeg * sizeof(SegCounter), s));
+  CK(cudaMemsetAsync(ctx->dcnt, 0, 2 * sizeof(uint32_t), s));
   CK(cudaEventRecord(ctx->ev[0], s));
   CK(launch_hash(kp, s, lo, hi));
   ctx->launches = 1;
