@@ -623,28 +623,35 @@ def run_sharded(args, world, rank, local):
     shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
                          max_batch_tokens=s.n_tokens + 64, max_batch_requests=per, seed=SEED,
                          device=local)
-    # The library's own exchange over peer memory: SOLID_DIST_EXCHANGE=p2p-dev
-    # (default: records stored into the peers' buffers by the pack kernels, device-resident
-    # counts) or p2p (host counts); =torch: torch.distributed (NCCL, or gloo with host staging).
-    # If some rank cannot map its peers (no CUDA IPC), every rank falls back to torch.
-    xport = os.environ.get("SOLID_DIST_EXCHANGE", "p2p-dev")
+    # Transport (SOLID_DIST_EXCHANGE): "native" (default) = the whole sharded admission as ONE
+    # C-ABI call, solid_dist_admit (agreement, rounds, commit and overflow vote
+    # inside the library over CUDA-IPC peer memory); "p2p-dev" / "p2p" = the same exchange
+    # driven from Python (device- / host-resident counts); "torch" = torch.distributed (NCCL, or
+    # gloo with host staging).  If some rank cannot map its peers, every rank falls back to torch.
+    xport = os.environ.get("SOLID_DIST_EXCHANGE", "native")
     ex = None
-    if xport in ("p2p", "p2p-dev"):
+
+    def make_shard():
+        return ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
+                            max_batch_tokens=s.n_tokens + 64, max_batch_requests=per, seed=SEED,
+                            device=local)
+
+    if xport in ("native", "p2p", "p2p-dev"):
         try:
             ex = PeerExchange(shard, device_counts=xport == "p2p-dev")
-            xname = "p2p (CUDA IPC peer stores + mailbox flags)" + (
-                ", device-resident counts" if xport == "p2p-dev" else "")
+            xname = {"native": "solid_dist_admit (one C-ABI call; CUDA IPC peer stores + mailbox "
+                               "flags, device-resident counts)",
+                     "p2p-dev": "p2p (CUDA IPC peer stores + mailbox flags), device-resident counts",
+                     "p2p": "p2p (CUDA IPC peer stores + mailbox flags)"}[xport]
         except PeerUnavailable as e:
             print(f"[bench] {e}; falling back to torch.distributed", file=sys.stderr)
-            shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
-                                 max_batch_tokens=s.n_tokens + 64, max_batch_requests=per,
-                                 seed=SEED, device=local)
+            shard = make_shard()
             xport = "torch"
     if ex is None:
         staging = os.environ.get("SOLID_DIST_BACKEND", "nccl") != "nccl"
         ex = TorchExchange(shard, staging=staging)
         xname = "gloo, host-staged" if staging else "nccl all_to_all + batched p2p"
-    coll = {"s": 0.0}
+    coll = {"s": 0.0, "bytes": 0, "exchanges": 0}
 
     def timed_exchange(counts, flags=None):
         torch.cuda.synchronize()
@@ -660,6 +667,12 @@ def run_sharded(args, world, rank, local):
         return r
 
     def step():
+        if xport == "native":
+            res, tm = ex.admit_native(d["tokens"], d["offsets"], d["users"], None, lo)
+            coll["s"] += tm.exchange_ms / 1e3      # device time in the exchange waits
+            coll["bytes"] += tm.recv_records_remote * tm.record_bytes
+            coll["exchanges"] += tm.exchanges
+            return res, tm.rounds
         if xport == "p2p-dev":
             return run_protocol_device(shard, (d["tokens"], d["offsets"], d["users"], None, lo),
                                        timed_exchange_dev, ex.allreduce_max)
@@ -672,14 +685,14 @@ def run_sharded(args, world, rank, local):
         step()
     torch.cuda.synchronize()
     cs = torch.cuda.current_stream(dev)
-    ms, rounds, colls = [], [], []
+    ms, rounds, colls, cbytes = [], [], [], []
     with ClockSampler(local) as clk:
         dist.barrier()
         torch.cuda.synchronize()
         for _ in range(args.steps):
             shard.index.reset()
             dist.barrier()
-            coll["s"] = 0.0
+            coll["s"], coll["bytes"], coll["exchanges"] = 0.0, 0, 0
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(cs)
             res, t = step()
@@ -688,15 +701,48 @@ def run_sharded(args, world, rank, local):
             ms.append(a.elapsed_time(b))
             rounds.append(t)
             colls.append(coll["s"] * 1e3)
+            cbytes.append(coll["bytes"])
         torch.cuda.synchronize()
         dist.barrier()
     clocks = clk.summary()
-    tot = torch.tensor([sum(ms), sum(colls)], dtype=torch.float64, device=dev)
+    tot = torch.tensor([sum(ms), sum(colls), sum(cbytes)], dtype=torch.float64, device=dev)
     dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     tot_ms, coll_ms = float(tot[0]), float(tot[1])
+    xbytes = torch.tensor([sum(cbytes)], dtype=torch.float64, device=dev)
+    dist.all_reduce(xbytes, op=dist.ReduceOp.SUM)
     value = per * world * args.steps / (tot_ms / 1e3)
     peak, peak_src = _peaks()
     alg = (64 * nblk + 37 * per) * world
+    # parity of the timed configuration: rank 0's slice is the first `per` requests of the global
+    # sequence, so its results depend on nothing else (R1) — the sequential oracle on that slice
+    # alone must give them exactly; every rank's results must also equal a second transport's
+    # (NCCL all-to-all-v through a second shard set) on the same batch
+    parity = {"rank0_vs_oracle": None, "transport": None}
+    mism = 0
+    if rank == 0 and not args.no_cpu:
+        from oracle import Oracle
+        o = Oracle(16, SEED, 2)
+        o.reserve(nblk // 8 + 1024)
+        exp = o.process(s)
+        got = P.as_numpy(res)
+        mism = sum(int((got[f] != exp[f]).sum()) for f in exp.dtype.names)
+        parity["rank0_vs_oracle"] = {"requests": per, "mismatches": mism}
+    if xport != "torch" and os.environ.get("SOLID_DIST_BACKEND", "nccl") == "nccl" and \
+            os.environ.get("SOLID_DIST_CHECK", "1") == "1":
+        first = P.as_numpy(res).copy()
+        shard2 = make_shard()
+        ex2 = TorchExchange(shard2)
+        r2, _ = ex2.admit(d["tokens"], d["offsets"], d["users"], None, lo)
+        torch.cuda.synchronize()
+        bad = torch.tensor([sum(int((P.as_numpy(r2)[f] != first[f]).sum())
+                                for f in first.dtype.names)], dtype=torch.int64, device=dev)
+        dist.all_reduce(bad, op=dist.ReduceOp.SUM)
+        parity["transport"] = {"other": "nccl all_to_all + batched p2p (TorchExchange)",
+                               "mismatches": int(bad.item())}
+        del shard2, ex2
+    parity["status"] = "exact" if (mism == 0 and (parity["transport"] is None or
+                                                  parity["transport"]["mismatches"] == 0)) \
+        else "MISMATCH"
     res_np = P.as_numpy(res)
     # e2e: the same sharded admission from pinned host buffers (H2D + admit + D2H per step)
     e2e = None
@@ -738,8 +784,18 @@ def run_sharded(args, world, rank, local):
                          "traffic": None, "peak_source": peak_src},
             "cpu_baseline": None,
             "e2e": e2e,
-            "gpu_launches": int(sum(7 + 8 * r for r in rounds)),   # begin 3 + ingest0 3 + commit 1; 8 per round
+            # begin 3 + REG 2 + ingest0 4 + PULL 2 + 15 per round (round 5, INT 2, ingest 6, PULL
+            # 2; no PULL after the last) + commit 2 + three value exchanges (native) 6
+            "gpu_launches": int(sum((17 if xport == "native" else 11) + 15 * r if xport != "torch"
+                                    else 9 + 11 * r for r in rounds)),
             "collectives_ms_per_step": coll_ms / args.steps,
+            "collectives": {"ms_per_step_max_rank": coll_ms / args.steps,
+                            "what": ("device time inside the exchange waits (post -> every peer "
+                                     "posted), from solid_dist_timing" if xport == "native" else
+                                     "host time around the exchange calls"),
+                            "remote_bytes_per_step_all_ranks": float(xbytes.item()) / args.steps,
+                            "exchanges_per_step": coll["exchanges"]},
+            "parity": parity,
             "resolver_rounds": rounds[-1],
             "clocks": clocks,
             "step_ms": ms,

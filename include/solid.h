@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SOLID_ABI_VERSION 6u
+#define SOLID_ABI_VERSION 7u
 #define SOLID_USER_NONE 0xFFFFFFFFu   /* "no user": sharer of an unflagged entry */
 
 typedef enum {
@@ -396,6 +396,40 @@ solid_status solid_dist_p2p_exchange(solid_ctx* ctx, uint32_t flag, uint64_t* re
 solid_status solid_dist_p2p_device_counts(solid_ctx* ctx, uint32_t on);
 solid_status solid_dist_p2p_exchange_dev(solid_ctx* ctx, uint32_t sync, uint32_t* gflag_out,
                                          void* stream);
+
+/* ---- The sharded admission as one call -------------
+ * Runs the whole protocol above inside the library over the peer-memory exchange: every rank
+ * calls it once per batch with its own slice (after solid_dist_p2p_export / _connect on every
+ * rank; the caller only all-gathers the 64-byte handles once).  Steps:
+ *   1. agreement: every rank posts (seq_base, n) and a "slice rejected" bit (null pointers,
+ *      n > max_batch_requests, misaligned tokens, sequence beyond 32 bits); slices must be
+ *      contiguous in rank order (seq_base[r] = seq_base[r-1] + n[r-1]).  Every rank sees the
+ *      same values, so every rank returns the same verdict: SOLID_ERR_INVALID (the rejecting
+ *      rank, or all ranks for non-contiguous slices) / SOLID_ERR_STATE (the other ranks);
+ *   2. begin -> REG -> owner registration -> PULL -> rounds t = 1, 2, ...: Detector round ->
+ *      INT (carries each rank's changed flag and device-error bit) -> intent reduction; stop at
+ *      the first t >= 2 with no change anywhere (APC / USER_ISOLATION: t = 1).  A device error
+ *      on any rank (invalid batch, scratch / exchange overflow) abandons the batch on every rank
+ *      at that round's INT exchange (the failing rank returns its own code, the others
+ *      SOLID_ERR_STATE); nothing is committed;
+ *   3. commit: each shard counts its new entries; a capacity overflow (or error) on any shard is
+ *      voted through one more exchange and every shard that claimed rolls back (SOLID_ERR_CAPACITY
+ *      on every rank; the index is as before the batch).
+ * A peer that does not post within 60 s -> SOLID_ERR_NCCL on the waiting ranks.
+ * Device pointers as in solid_dist_begin; out[n] = this slice's results.  `timing` (may be NULL)
+ * receives the rounds and the exchange figures of this call.  Synchronises `stream`. */
+typedef struct {
+  uint32_t rounds;               /* resolver rounds                                          */
+  uint32_t exchanges;            /* record exchanges (REG, PULL, INT)                        */
+  float exchange_ms;             /* device time in the exchange waits (post -> every peer
+                                    posted; includes waiting for the slowest rank)           */
+  uint32_t record_bytes;         /* bytes per record (24)                                    */
+  uint64_t recv_records_remote;  /* records received from other ranks over the whole batch  */
+  uint64_t recv_records_local;   /* records this rank sent itself                            */
+} solid_dist_timing;
+
+solid_status solid_dist_admit(solid_ctx* ctx, const solid_batch* local, solid_result* out,
+                              uint64_t seq_base, solid_dist_timing* timing, void* stream);
 
 #ifdef __cplusplus
 }

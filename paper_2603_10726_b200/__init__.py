@@ -36,7 +36,7 @@ ABI_SYMBOLS = ["solid_abi_version", "solid_init", "solid_destroy", "solid_lookup
                "solid_dist_buffers", "solid_dist_counts", "solid_dist_begin",
                "solid_dist_owner_ingest", "solid_dist_round", "solid_dist_commit",
                "solid_dist_p2p_export", "solid_dist_p2p_connect", "solid_dist_p2p_exchange",
-               "solid_dist_p2p_device_counts", "solid_dist_p2p_exchange_dev",
+               "solid_dist_p2p_device_counts", "solid_dist_p2p_exchange_dev", "solid_dist_admit",
                "solid_activator_init", "solid_activator_destroy", "solid_activator_run",
                "solid_activator_last_error"]
 RECORD_BYTES = 24   # sharded-mode exchange record

@@ -161,6 +161,16 @@ def loopback_admit(shards: List[ShardedIndex], local_batches, seq_bases):
     return run_protocol(shards, args, exchange, lambda xs: max(xs))
 
 
+class DistTiming(ctypes.Structure):
+    """solid_dist_timing (include/solid.h): rounds and exchange figures of one admission."""
+    _fields_ = [("rounds", ctypes.c_uint32), ("exchanges", ctypes.c_uint32),
+                ("exchange_ms", ctypes.c_float), ("record_bytes", ctypes.c_uint32),
+                ("recv_records_remote", ctypes.c_uint64), ("recv_records_local", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 class PeerUnavailable(RuntimeError):
     """Some rank could not map its peers' regions (no CUDA IPC / peer access): raised on every
     rank alike, so callers can fall back to another transport together."""
@@ -230,6 +240,29 @@ class PeerExchange:
         sh.index._check(sh.index.lib.solid_dist_p2p_exchange_dev(
             sh.index.h, 1 if sync else 0, ctypes.byref(g), Index._stream(None)))
         return int(g.value)
+
+    def admit_native(self, tokens, offsets, users, enforce=None, seq_base: int = 0):
+        """The whole sharded admission as ONE C-ABI call (solid_dist_admit): agreement on the
+        slices, rounds, commit and overflow vote run inside the library over peer memory.
+        Returns (results tensor, DistTiming)."""
+        import torch
+        from . import _Batch
+        sh = self.shard
+        lib, h = sh.index.lib, sh.index.h
+        if not getattr(lib, "_dist_admit_typed", False):
+            lib.solid_dist_admit.restype = ctypes.c_int
+            lib.solid_dist_admit.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+            lib._dist_admit_typed = True
+        n = int(users.numel())
+        sh.out = torch.empty((max(n, 1), 6), dtype=torch.int32, device=offsets.device)
+        sh.n = n
+        b = _Batch(n, tokens.data_ptr(), offsets.data_ptr(), users.data_ptr(),
+                   enforce.data_ptr() if enforce is not None else None)
+        tm = DistTiming()
+        sh.index._check(lib.solid_dist_admit(h, ctypes.byref(b), ctypes.c_void_p(sh.out.data_ptr()),
+                                             seq_base, ctypes.byref(tm), Index._stream(None)))
+        return sh.results(), tm
 
     def admit(self, tokens, offsets, users, enforce=None, seq_base: int = 0):
         if not self.device_counts:

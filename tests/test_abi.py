@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol(lib):
     for name in _declared():
         assert hasattr(lib, name), name
     lib.solid_abi_version.restype = ctypes.c_uint32
-    assert lib.solid_abi_version() == 6
+    assert lib.solid_abi_version() == 7
 
 
 def test_binding_symbols_match_header():
