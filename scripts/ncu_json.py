@@ -1,6 +1,9 @@
 """Per-kernel summary (µs, DRAM bytes) of an ncu launch list -> profiles/latest_ncu.json.
 
-  python scripts/ncu_json.py gpurun_out/launches.csv profiles/r01/launches_c2.csv > profiles/latest_ncu.json
+  python scripts/ncu_json.py gpurun_out/launches.csv profiles/r02/launches_c2.csv [commit] > profiles/latest_ncu.json
+
+The Activator section of the previous profiles/latest_ncu.json is carried over (its kernels are
+profiled by scripts/profile_activator.sh).
 
 Only launches of the second bench step are kept (the first step includes one-time setup)."""
 import csv
@@ -23,8 +26,10 @@ hashes = [k for k, (i, n, m) in enumerate(launches) if n == "k_hash_register"]
 second = launches[hashes[1]:] if len(hashes) > 1 else launches
 unit = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-out = {"source": f"{sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]}: ncu --metrics "
-                 "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+commit = sys.argv[3] if len(sys.argv) > 3 else "unknown"
+out = {"source": f"{sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]} (commit {commit}): ncu --metrics "
+                 "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
+                 "lts__t_sector_hit_rate.pct,smsp__inst_executed.sum "
                  "--clock-control none, bench.py --profile --steps 1 --warmup 1 (C2, second step)",
        "kernels": OrderedDict()}
 for i, n, m in second:
@@ -40,4 +45,10 @@ for i, n, m in second:
     if "dram_read" in d and "dram_write" in d:
         d["traffic"] = d["dram_read"] + d["dram_write"]
     out["kernels"].setdefault(n, []).append(d)
+try:
+    prev = json.load(open("profiles/latest_ncu.json"))
+    if "activator" in prev:
+        out["activator"] = prev["activator"]
+except (OSError, ValueError):
+    pass
 print(json.dumps(out, indent=1))
