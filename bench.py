@@ -620,7 +620,7 @@ def run_sharded(args, world, rank, local):
     nblk = s.n_blocks()
     dev = torch.device("cuda", local)
     d = P.to_device(s, dev)
-    shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
+    shard = ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 6, 1 << 20),
                          max_batch_tokens=s.n_tokens + 64, max_batch_requests=per, seed=SEED,
                          device=local)
     # Transport (SOLID_DIST_EXCHANGE): "native" (default) = the whole sharded admission as ONE
@@ -632,7 +632,7 @@ def run_sharded(args, world, rank, local):
     ex = None
 
     def make_shard():
-        return ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 4, 1 << 20),
+        return ShardedIndex(world, rank, "solidarity", capacity_blocks=max(nblk // 6, 1 << 20),
                             max_batch_tokens=s.n_tokens + 64, max_batch_requests=per, seed=SEED,
                             device=local)
 

@@ -80,6 +80,8 @@ struct DevStatus {
   unsigned long long live_after;         // asynchronous admission: live entries after this batch
   unsigned long long ids_after_hash;     // distinct keys registered by K_A (its snapshot probes)
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
+  uint32_t fast_commit;                  // k_stats: live + registered ids <= capacity, so the
+                                         // batch cannot overflow: k_commit counts and updates live
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t seg[kNSeg];                   // id counts per segment (gathered by k_stats)
 #ifdef SOLID_COUNTERS
@@ -144,6 +146,7 @@ struct KParams {
   ulonglong2* lint;                // per local id: the intents last sent to its owner (delta INT)
   uint32_t* long_q;                // K_A: requests longer than kLongBlocks (CTA path)
   uint32_t* pool_cnt;              // block_table: k_commit counts each request's new entries
+  uint32_t* seg_new;               // [kNSeg][2] fast_commit: k_commit's new entries / sharers
   // LRU eviction mode (solid_evict.inc): keys of the batch whose LRU record lies
   // in the eviction window get a window index w (their index snapshot is then visible only up
   // to their eviction time win_ev[w]); winfo[id] = epoch << 32 | w publishes an id's creation
@@ -1187,8 +1190,9 @@ __device__ __forceinline__ uint32_t final_round(const KParams& kp) {
   return kp.st->conv == 0 ? 0 : (POLICY_IS_SOLIDARITY(kp) ? kp.st->conv : 0);
 }
 
-__global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
+__global__ void __launch_bounds__(256, 5) k_commit(KParams kp, int mode) {
   constexpr int U = 4;                 // ids per thread, staged so all loads are in flight at once
+  uint32_t n_ins = 0, n_flg = 0;       // fast_commit: this thread's new entries / sharer writes
   // the converged round is read on the device (lookup never waits for the host); an invalid,
   // unconverged or over-capacity batch commits nothing
   if (kp.st->err || (kp.n && kp.st->conv == 0)) return;
@@ -1231,6 +1235,7 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
       const uint32_t itag = (uint32_t)(pw[q].x >> 32);
       if (itag == tag) {
         Cold* c = kp.cold + id;
+        ++n_ins;
         if (mode == 1 && kp.pool_cnt) atomicAdd(&kp.pool_cnt[(uint32_t)pw[q].x - 1u], 1u);
         if (mode == 1) {
           const ulonglong2 val =
@@ -1247,11 +1252,51 @@ __global__ void __launch_bounds__(256) k_commit(KParams kp, int mode) {
         }
       } else if (itag == tagS && (uint32_t)(pw[q].y >> 32) == tag) {
         uint32_t* sharer_word = reinterpret_cast<uint32_t*>(&kp.tab[kp.cold[id].psl].y) + 1;
+        ++n_flg;
         if (mode == 1) atomicCAS(sharer_word, kNone, who[q]);
         else atomicCAS(sharer_word, who[q], kNone);
       }
     }
   }
+  // fast_commit (k_stats skipped its count: this batch cannot overflow): the commit counts the
+  // batch's new entries and sharer writes itself (k_live then advances the live count)
+  if (mode != 1 || !kp.st->fast_commit) return;
+  for (int o = 16; o; o >>= 1) {       // one reduction per warp (no CTA barrier: registers)
+    n_ins += __shfl_xor_sync(0xffffffffu, n_ins, o);
+    n_flg += __shfl_xor_sync(0xffffffffu, n_flg, o);
+  }
+  if ((threadIdx.x & 31) == 0) {       // per-segment counters: no hot same-address atomics
+    if (n_ins) atomicAdd(&kp.seg_new[2 * seg], n_ins);
+    if (n_flg) atomicAdd(&kp.seg_new[2 * seg + 1], n_flg);
+  }
+}
+
+// After k_commit, fast_commit only: the batch's new entries / sharer writes from k_commit's
+// per-segment counts; live += new entries.
+__global__ void k_live(DevStatus* st, unsigned long long* live, const uint32_t* seg_new) {
+  if (!st->fast_commit) return;
+  const int q = threadIdx.x;           // kNSeg threads
+  unsigned long long a = seg_new[2 * q], b = seg_new[2 * q + 1];
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __shared__ unsigned long long s_a[kNSeg / 32], s_b[kNSeg / 32];
+  if ((q & 31) == 0) {
+    s_a[q >> 5] = a;
+    s_b[q >> 5] = b;
+  }
+  __syncthreads();
+  if (q) return;
+  a = b = 0;
+  for (int w = 0; w < kNSeg / 32; ++w) {
+    a += s_a[w];
+    b += s_b[w];
+  }
+  st->new_entries = a;
+  st->new_flags = b;
+  *live += a;
+  st->live_after = *live;
 }
 
 // K_D, before the commit: per-batch sums over the results (block-weighted hit rate) and
@@ -1263,7 +1308,13 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
                                                DevStatus* st, unsigned long long* live,
                                                unsigned long long cap, const SegCounter* seg,
                                                KParams kp) {
-  if (blockIdx.x == 0 && threadIdx.x < kNSeg) st->seg[threadIdx.x] = seg[threadIdx.x].v;
+  if (blockIdx.x == 0 && threadIdx.x < kNSeg) {
+    st->seg[threadIdx.x] = seg[threadIdx.x].v;
+    if (kp.seg_new) {
+      kp.seg_new[2 * threadIdx.x] = 0;   // k_commit's per-segment counts (fast_commit)
+      kp.seg_new[2 * threadIdx.x + 1] = 0;
+    }
+  }
   unsigned long long a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
@@ -1276,6 +1327,7 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
     a[5] += 1;
   }
   const bool ok = live && !st->err && !(n && st->conv == 0);
+  bool fast = false;
   if (ok) {                            // new entries (a[6]) and new sharer writes (a[7])
     // flat index over every registered id: segment prefix sums in shared memory, so each thread
     // handles ~ids / threads ids with independent loads (no per-segment serial loop)
@@ -1290,9 +1342,13 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
     const int W = (int)(tf & 1);
     const uint32_t tag = tag_of(kp.epoch, tf), tagS = tag_of(kp.epoch, kSubSnap);
     const uint32_t total = s_pre[kNSeg];
+    // every new entry has a registered id: when even all of them fit, the batch cannot
+    // overflow — skip this counting pass; k_commit counts while it claims (fast_commit)
+    fast = *(volatile unsigned long long*)live + total <= cap;
     constexpr int UQ = 4;                    // ids per thread per step, loads in flight together
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t g0 = blockIdx.x * blockDim.x + threadIdx.x; g0 < total; g0 += UQ * stride) {
+    for (uint32_t g0 = blockIdx.x * blockDim.x + threadIdx.x; g0 < (fast ? 0u : total);
+         g0 += UQ * stride) {
       ulonglong2 pw[UQ];
 #pragma unroll
       for (int q = 0; q < UQ; ++q) {
@@ -1335,7 +1391,9 @@ __global__ void __launch_bounds__(256) k_stats(const solid_result* out, uint64_t
   __syncthreads();
   if (!s_last || threadIdx.x != 0) return;
   __threadfence();
-  if (ok) {
+  if (ok && fast) {
+    st->fast_commit = 1;               // k_commit counts (seg_new), k_live advances live
+  } else if (ok) {
     const unsigned long long l = *live, add = *(volatile unsigned long long*)&st->new_entries;
     if (l + add > cap) st->overflow = 1;
     else *live = l + add;
@@ -1453,6 +1511,7 @@ struct solid_ctx {
   uint64_t launches = 0;
   uint64_t resolve_ctas = 0;
   unsigned long long* live_dev = nullptr;   // live count for the asynchronous admission path
+  uint32_t* seg_new = nullptr;               // [kNSeg][2] fast-commit counts (k_commit)
   // batches in flight: a ring of kRing status slots (pinned host mirrors + events); the
   // asynchronous ones wait in [head, head + outstanding) for solid_batch_status
   HostSlot* slots = nullptr;
@@ -1542,6 +1601,7 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->seg_cnt);
   cudaFree(c->st);
   cudaFree(c->live_dev);
+  cudaFree(c->seg_new);
   cudaFree(c->mpow);
   cudaFree(c->gtab);
   cudaFree(c->long_q);
@@ -1643,6 +1703,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
             alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(SegCounter)) &&
             alloc((void**)&ctx->st, sizeof(DevStatus)) &&
             alloc((void**)&ctx->live_dev, sizeof(unsigned long long)) &&
+            alloc((void**)&ctx->seg_new, 2 * kNSeg * sizeof(uint32_t)) &&
             alloc((void**)&ctx->mpow, mb * sizeof(unsigned long long)) &&
             alloc((void**)&ctx->gtab, (mb + 1) * sizeof(unsigned long long)) &&
             alloc((void**)&ctx->long_q, (cfg->max_batch_requests + 1) * sizeof(uint32_t)) &&
@@ -1773,6 +1834,7 @@ static solid_status launch_resolve(solid_ctx* ctx, cudaStream_t s) {
 
 static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
   k_commit<<<dim3(16, kNSeg), 256, 0, s>>>(c->kp, mode);   // 4 staged ids per thread
+  if (mode == 1) k_live<<<1, kNSeg, 0, s>>>(c->st, c->live_dev, c->seg_new);
 }
 
 // Validates the batch and prepares the kernel parameters of a lookup (no kernel launched yet).
@@ -1853,6 +1915,7 @@ static solid_status lookup_setup(solid_ctx* ctx, const solid_batch* b, solid_res
   // the per-step CTA barriers cost more than they parallelise (C3: 1.64 vs 1.34 ms)
   kp.long_q = b->n_requests <= kLongMaxBatch ? ctx->long_q : nullptr;
   kp.pool_cnt = ctx->pool_cnt;
+  kp.seg_new = ctx->seg_new;
   kp.seg_cnt = ctx->seg_cnt;
   kp.seg_cap = ctx->seg_cap;
   kp.st = ctx->st;
@@ -1919,13 +1982,14 @@ static solid_status enqueue_commit(solid_ctx* ctx, cudaStream_t s) {
   if (n) {
     if (ctx->kp.pool_cnt) CK(cudaMemsetAsync(ctx->kp.pool_cnt, 0, ctx->kp.n * 4, s));
     // counts and the capacity decision first (device-resident live count), then the claims
-    k_stats<<<1184, 256, 0, s>>>(   // 148 SMs x 8: the id count spans every registered key
+    k_stats<<<296, 256, 0, s>>>(    // 148 SMs x 2: the id count spans every registered key
+                                    // (more CTAs only add same-address atomics)
         ctx->kp.out + ctx->kp.j_lo, n, ctx->st, ctx->live_dev, ctx->cfg.capacity_blocks,
         ctx->seg_cnt, ctx->kp);
     CK(cudaGetLastError());
     launch_commit(ctx, 1, s);
     CK(cudaGetLastError());
-    ctx->launches += 2;
+    ctx->launches += 3;
   }
   CK(cudaEventRecord(ctx->ev[3], s));
   CK(cudaMemcpyAsync(ctx->st_host, ctx->st, kStHead, cudaMemcpyDeviceToHost, s));
