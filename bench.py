@@ -1012,11 +1012,30 @@ def main():
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             assert (hout["reused"] == res["reused"]).all()
             e2e_u32 = e2e
+            # the bound: the same bytes as one plain pinned host->device copy (PCIe)
+            hb = int(h16.nbytes + ho.nbytes + hu.nbytes)
+            src = torch.from_numpy(h16.view(np.uint8)).pin_memory()
+            dst = torch.empty(src.numel(), dtype=torch.uint8, device=dev)
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            cps = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                dst.copy_(src, non_blocking=True)
+                torch.cuda.synchronize()
+                cps.append(time.perf_counter() - t0)
+            copy_gbps = src.numel() / min(cps) / 1e9
+            del src, dst
+            e2e_s = float(tt.item()) / args.e2e_steps
             e2e = {"value": reqs_all * args.e2e_steps / float(tt.item()), "unit": "requests/s",
-                   "h2d_bytes_per_step": int(h16.nbytes + ho.nbytes + hu.nbytes),
+                   "h2d_bytes_per_step": hb,
                    "d2h_bytes_per_step": int(hout.nbytes), "token_bits": 16,
                    "how": "solid_admit_host_u16: pinned host buffers (16-bit token ids) -> H2D -> "
                           "widen on the device -> lookup -> insert -> D2H, host wall clock",
+                   "bound": {"what": "PCIe host->device copy of the step's inputs",
+                             "h2d_gbps_achieved": hb / e2e_s / 1e9,
+                             "h2d_gbps_plain_copy": copy_gbps,
+                             "frac": (hb / copy_gbps / 1e9) / e2e_s},
                    "u32_tokens": e2e_u32}
 
     activator = None
