@@ -756,7 +756,8 @@ def run_sharded(args, world, rank, local):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             dt, do, du = ht.to(dev, non_blocking=True), ho.to(dev, non_blocking=True), hu.to(dev, non_blocking=True)
-            r = [ex.admit(dt, do, du, None, lo)[0]]
+            r = [ex.admit_native(dt, do, du, None, lo)[0] if xport == "native"
+                 else ex.admit(dt, do, du, None, lo)[0]]
             r[0].cpu()
             et += time.perf_counter() - t0
         tt = torch.tensor([et], dtype=torch.float64, device=dev)
