@@ -8,10 +8,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "solid.cu"), os.path.join(PKG, "csrc", "solid_activator.cu")]
-DEPS = SRC + [os.path.join(PKG, "csrc", "solid_math.cuh"), os.path.join(PKG, "csrc", "solid_dist.inc"),
-               os.path.join(PKG, "csrc", "solid_evict.inc"), os.path.join(PKG, "csrc", "solid_pool.inc"),
-               os.path.join(PKG, "csrc", "solid_p2p.inc"),
-               os.path.join(ROOT, "include", "solid.h")]
+DEPS = SRC + sorted(os.path.join(PKG, "csrc", f) for f in os.listdir(os.path.join(PKG, "csrc"))
+                    if f.endswith((".inc", ".cuh"))) + [os.path.join(ROOT, "include", "solid.h")]
 LIB = os.path.join(PKG, "lib", "libsolid.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -145,6 +145,12 @@ struct KParams {
   uint32_t* mown;                  // per local id: owner user of the mirrored first inserter
   ulonglong2* lint;                // per local id: the intents last sent to its owner (delta INT)
   uint32_t* long_q;                // K_A: requests longer than kLongBlocks (CTA path)
+  // packed K_A for short requests (solid_pack.inc): on for whole-batch launches only
+  int pack;
+  uint32_t* pk_pre;                // [n + 1] packed full-block prefix Bp[j]
+  uint32_t* pk_ctot;               // [grid] per-CTA chunk totals
+  uint32_t* pk_cpre;               // [grid + 1] their exclusive prefix
+  uint32_t* pk_wfirst;             // [warps + 2] first request starting in each warp's span
   uint32_t* pool_cnt;              // block_table: k_commit counts each request's new entries
   uint32_t* seg_new;               // [kNSeg][2] fast_commit: k_commit's new entries / sharers
   // LRU eviction mode (solid_evict.inc): keys of the batch whose LRU record lies
@@ -555,8 +561,11 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
   return bad;
 }
 
+__device__ __forceinline__ bool pack_chosen(const KParams& kp);
+
 template <int POLICY, int NC>
 __global__ void __launch_bounds__(256, 4) k_hash_register(KParams kp, uint64_t j_lo, uint64_t j_hi) {
+  if (pack_chosen(kp)) return;           // short requests: k_hash_packed registers the batch
   const int lane = threadIdx.x & 31;
   const uint64_t j = j_lo + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (j >= j_hi) return;
@@ -718,6 +727,8 @@ static cudaError_t launch_hash(const KParams& kp, cudaStream_t s, uint64_t lo, u
 static cudaError_t launch_hash(const KParams& kp, cudaStream_t s) {
   return launch_hash(kp, s, 0, kp.n);
 }
+
+#include "solid_pack.inc"
 
 // ---------------------------------------------------------------------------------------------
 // K_B: one resolver round t (t >= 1) — the per-request Detector of P:454-459 evaluated against
@@ -1473,6 +1484,12 @@ struct solid_ctx {
   uint32_t stamp_wait_ns = kStampWaitNs;
   uint32_t* dlist = nullptr;
   uint32_t* dcnt = nullptr;
+  int pack = 1;                          // packed K_A for short requests (SOLID_PACK=0: off)
+  uint32_t* pk_pre = nullptr;
+  uint32_t* pk_ctot = nullptr;
+  uint32_t* pk_cpre = nullptr;
+  uint32_t* pk_wfirst = nullptr;
+  uint32_t pk_grid = 0;                  // its cooperative grid (resident CTAs)
   SegCounter* seg_cnt = nullptr;
   uint32_t seg_cap = 0;
   DevStatus* st = nullptr;
@@ -1598,6 +1615,10 @@ static void free_all(solid_ctx* c) {
   cudaFree(c->fst);
   cudaFree(c->dlist);
   cudaFree(c->dcnt);
+  cudaFree(c->pk_pre);
+  cudaFree(c->pk_ctot);
+  cudaFree(c->pk_cpre);
+  cudaFree(c->pk_wfirst);
   cudaFree(c->seg_cnt);
   cudaFree(c->st);
   cudaFree(c->live_dev);
@@ -1665,6 +1686,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   ctx->cfg.world = world;
   ctx->dev = cfg->device;
   if (const char* e = getenv("SOLID_STAMP")) ctx->stamp_rule = atoi(e) != 0;
+  if (const char* e = getenv("SOLID_PACK")) ctx->pack = atoi(e) != 0;
   if (const char* e = getenv("SOLID_STAMP_WAIT")) ctx->stamp_wait_ns = (uint32_t)atoi(e);
   if (const char* e = getenv("SOLID_RESOLVE_TILE")) {
     const int v = atoi(e);
@@ -1700,6 +1722,10 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
             alloc((void**)&ctx->fst, std::max<uint64_t>(cfg->max_batch_requests, 1) * sizeof(unsigned long long)) &&
             alloc((void**)&ctx->dlist, std::max<uint64_t>(cfg->max_batch_requests, 1) * sizeof(uint32_t)) &&
             alloc((void**)&ctx->dcnt, 2 * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->pk_pre, (cfg->max_batch_requests + 2) * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->pk_ctot, 8192 * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->pk_cpre, 8193 * sizeof(uint32_t)) &&
+            alloc((void**)&ctx->pk_wfirst, (ctx->slot_cap / kPackSpan + 4) * sizeof(uint32_t)) &&
             alloc((void**)&ctx->seg_cnt, kNSeg * sizeof(SegCounter)) &&
             alloc((void**)&ctx->st, sizeof(DevStatus)) &&
             alloc((void**)&ctx->live_dev, sizeof(unsigned long long)) &&
@@ -1914,6 +1940,7 @@ static solid_status lookup_setup(solid_ctx* ctx, const solid_batch* b, solid_res
   // resident warps (148 SMs x 32): with more, warp-per-request already fills the machine and
   // the per-step CTA barriers cost more than they parallelise (C3: 1.64 vs 1.34 ms)
   kp.long_q = b->n_requests <= kLongMaxBatch ? ctx->long_q : nullptr;
+  kp.pack = 0;                     // set by do_lookup for its whole-batch K_A launch only
   kp.pool_cnt = ctx->pool_cnt;
   kp.seg_new = ctx->seg_new;
   kp.seg_cnt = ctx->seg_cnt;
@@ -1944,6 +1971,40 @@ static solid_status lookup_resolve(solid_ctx* ctx, cudaStream_t s) {
   return SOLID_OK;
 }
 
+static solid_status launch_hash_packed(solid_ctx* ctx, cudaStream_t s) {
+  KParams& kp = ctx->kp;
+  const void* fn;
+  const bool two = kp.nc == 2;
+  switch (ctx->cfg.policy) {
+    case SOLID_POLICY_APC:
+      fn = two ? (const void*)k_hash_packed<SOLID_POLICY_APC, 2>
+               : (const void*)k_hash_packed<SOLID_POLICY_APC, 1>;
+      break;
+    case SOLID_POLICY_USER_ISOLATION:
+      fn = two ? (const void*)k_hash_packed<SOLID_POLICY_USER_ISOLATION, 2>
+               : (const void*)k_hash_packed<SOLID_POLICY_USER_ISOLATION, 1>;
+      break;
+    default:
+      fn = two ? (const void*)k_hash_packed<SOLID_POLICY_SOLIDARITY, 2>
+               : (const void*)k_hash_packed<SOLID_POLICY_SOLIDARITY, 1>;
+      break;
+  }
+  if (!ctx->pk_grid) {
+    int per_sm = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+    ctx->pk_grid = (uint32_t)std::min<int64_t>(std::max(per_sm, 1) * (int64_t)sms, 8192);
+  }
+  kp.pack = 1;
+  kp.pk_pre = ctx->pk_pre;
+  kp.pk_ctot = ctx->pk_ctot;
+  kp.pk_cpre = ctx->pk_cpre;
+  kp.pk_wfirst = ctx->pk_wfirst;
+  void* args[] = {(void*)&kp};
+  CK(cudaLaunchCooperativeKernel(fn, dim3(ctx->pk_grid), dim3(256), args, 0, s));
+  return SOLID_OK;
+}
+
 static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result* out,
                              void* stream) {
   solid_status rc = lookup_setup(ctx, b, out, stream);
@@ -1952,8 +2013,16 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   if (ctx->ev_state) return evict_lookup(ctx, s);
   CK(cudaEventRecord(ctx->ev[0], s));
   if (ctx->kp.n) {
+    if (ctx->pack && ctx->kp.n >= 2) {
+      // packed K_A (solid_pack.inc): taken on the device when requests are short; the
+      // warp-per-request K_A launched next exits at once then (and vice versa)
+      solid_status rc = launch_hash_packed(ctx, s);
+      if (rc != SOLID_OK) return rc;
+      ctx->launches += 1;
+    }
     CK(launch_hash(ctx->kp, s));
-    ctx->launches = 1;
+    ctx->kp.pack = 0;                    // later launches of this batch (splits) are per range
+    ctx->launches += 1;
   }
   return lookup_resolve(ctx, s);
 }
