@@ -80,6 +80,7 @@ struct DevStatus {
   unsigned long long live_after;         // asynchronous admission: live entries after this batch
   unsigned long long ids_after_hash;     // distinct keys registered by K_A (its snapshot probes)
   unsigned long long sums[6];            // blocks, reused, flagged, diverted, truncated, requests
+  uint32_t packed;                       // K_A: the packed kernel took this batch (short requests)
   uint32_t fast_commit;                  // k_stats: live + registered ids <= capacity, so the
                                          // batch cannot overflow: k_commit counts and updates live
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
@@ -1490,6 +1491,8 @@ struct solid_ctx {
   uint32_t* pk_cpre = nullptr;
   uint32_t* pk_wfirst = nullptr;
   uint32_t pk_grid = 0;                  // its cooperative grid (resident CTAs)
+  int pack_hint = 1;                     // the last collected batch took the packed K_A
+  uint32_t pack_probe = 0;               // batches since the packed kernel was last launched
   SegCounter* seg_cnt = nullptr;
   uint32_t seg_cap = 0;
   DevStatus* st = nullptr;
@@ -2013,9 +2016,13 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   if (ctx->ev_state) return evict_lookup(ctx, s);
   CK(cudaEventRecord(ctx->ev[0], s));
   if (ctx->kp.n) {
-    if (ctx->pack && ctx->kp.n >= 2) {
-      // packed K_A (solid_pack.inc): taken on the device when requests are short; the
-      // warp-per-request K_A launched next exits at once then (and vice versa)
+    // packed K_A (solid_pack.inc): taken on the device when requests are short; the
+    // warp-per-request K_A launched next exits at once then (and vice versa).  While collected
+    // batches do not take it, it is launched only every 64th batch (its early exit costs a
+    // cooperative launch; without it the warp-per-request K_A handles any batch by itself)
+    const bool try_pack = ctx->pack_hint || ++ctx->pack_probe >= 64;
+    if (ctx->pack && ctx->kp.n >= 2 && try_pack) {
+      ctx->pack_probe = 0;
       solid_status rc = launch_hash_packed(ctx, s);
       if (rc != SOLID_OK) return rc;
       ctx->launches += 1;
@@ -2113,6 +2120,7 @@ static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, boo
     S.live_entries = ctx->live;
   }
   S.last_rounds = ctx->rounds;
+  ctx->pack_hint = h.packed ? 1 : (f.n ? 0 : ctx->pack_hint);
   for (int q = 0; q < 8; ++q)
     S.round_us[q] = (q < (int)ctx->rounds && q < 16 && h.round_ns[q + 1] > h.round_ns[0])
                         ? (float)((h.round_ns[q + 1] - h.round_ns[q]) * 1e-3)
