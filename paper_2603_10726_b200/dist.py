@@ -200,6 +200,13 @@ class PeerExchange:
         allh = [None] * shard.world
         dist.all_gather_object(allh, bytes(mine.raw) if ok else b"", group=self.group)
         ok = all(len(x) == 64 for x in allh)
+        # every pair of GPUs must have peer access (NVLink / NVSwitch, or PCIe P2P); ranks on the
+        # same device map each other's buffers directly
+        import torch
+        devs = [None] * shard.world
+        dist.all_gather_object(devs, int(shard.index.device), group=self.group)
+        me = int(shard.index.device)
+        ok = ok and all(d == me or torch.cuda.can_device_access_peer(me, d) for d in devs)
         if ok:
             table = ctypes.create_string_buffer(b"".join(allh), 64 * shard.world)
             ok = lib.solid_dist_p2p_connect(h, table) == SOLID_OK
