@@ -70,6 +70,7 @@ def _parity_worker(rank, world, port, name, policy, outdir):
 
 @pytest.mark.parametrize("name,policy,world", [("c1", "solidarity", 2),
                                                ("c2_small", "solidarity", 3),
+                                               ("c2_small", "solidarity", 4),
                                                ("random", "solidarity", 2),
                                                ("random", "apc", 3),
                                                ("random", "user_isolation", 2)])
