@@ -1493,6 +1493,7 @@ struct solid_ctx {
   uint32_t pk_grid = 0;                  // its cooperative grid (resident CTAs)
   int pack_hint = 1;                     // the last collected batch took the packed K_A
   uint32_t pack_probe = 0;               // batches since the packed kernel was last launched
+  uint64_t pack_last_n = 0;              // batch size at the last launch decision
   SegCounter* seg_cnt = nullptr;
   uint32_t seg_cap = 0;
   DevStatus* st = nullptr;
@@ -2018,9 +2019,13 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
   if (ctx->kp.n) {
     // packed K_A (solid_pack.inc): taken on the device when requests are short; the
     // warp-per-request K_A launched next exits at once then (and vice versa).  While collected
-    // batches do not take it, it is launched only every 64th batch (its early exit costs a
-    // cooperative launch; without it the warp-per-request K_A handles any batch by itself)
-    const bool try_pack = ctx->pack_hint || ++ctx->pack_probe >= 64;
+    // batches do not take it, it is launched only when the batch size changed by more than 1.5x
+    // or every 64th batch (its early exit costs a cooperative launch; without it the
+    // warp-per-request K_A handles any batch by itself)
+    const uint64_t nn = ctx->kp.n;
+    const bool resized = nn * 2 < ctx->pack_last_n * 3 ? nn * 3 < ctx->pack_last_n * 2 : true;
+    const bool try_pack = ctx->pack_hint || resized || ++ctx->pack_probe >= 64;
+    ctx->pack_last_n = nn;
     if (ctx->pack && ctx->kp.n >= 2 && try_pack) {
       ctx->pack_probe = 0;
       solid_status rc = launch_hash_packed(ctx, s);
