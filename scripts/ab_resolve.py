@@ -45,7 +45,7 @@ def main():
         blocks = s.n_blocks() + sum(w.n_blocks() for w in pre)
         ref = None
         for v in a.variants:
-            env = dict(kv.split("=", 1) for kv in v.split(",") if kv)
+            env = dict(kv.split("=", 1) for kv in v.split(",") if kv and not kv.startswith("lib="))
             old = {k: os.environ.get(k) for k in env}
             os.environ.update(env)
             idx = P.Index("solidarity", capacity_blocks=max(blocks, 1 << 20), max_batch_tokens=mt,
