@@ -56,6 +56,34 @@ def _workload(name: str, rank: int):
     raise SystemExit(f"unknown config {name}")
 
 
+def config_n1(desc: str, n_req: int, n_blk: int, n_tok: int) -> dict:
+    """The N = 1 line's `config` (shared by both arms, so the driver compares like with like)."""
+    return {"workload": desc, "policy": "solidarity", "batch_requests": n_req,
+            "blocks_per_batch": n_blk, "tokens_per_batch": n_tok,
+            "parallelism": "1 independent tenant partitions (weak)",
+            "l2": "inputs (800 MB tokens) larger than L2 (126 MB); no flush",
+            "restore": "index reset to empty before every step, outside the events "
+                       "(stream-ordered between consecutive steps)",
+            "submission": "solid_admit_batch pipelined: step k+1 enqueued before "
+                          "step k's status is collected"}
+
+
+def sharded_shape(config: str, world: int):
+    """Requests per GPU and users of the N > 1 (weak-scaling) workload."""
+    per = 100_000 if config == "c2" else 10_000
+    users = (1000 if config == "c2" else 100) * world
+    return per, users
+
+
+def config_sharded(world: int, users: int, per: int) -> dict:
+    """The N > 1 line's `config` (shared by both arms; the transport is reported beside it)."""
+    return {"workload": f"c2_shared_prompt x{world}: {users} users x 100 requests, "
+                        f"2000-token prompts, {per} requests per GPU",
+            "policy": "solidarity", "parallelism": f"key-hash-sharded index over "
+            f"{world} GPUs, record exchange per resolver round",
+            "l2": "inputs larger than L2", "restore": "index reset before each step"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -573,6 +601,11 @@ def run_reference(args):
     from oracle import Oracle
     n_sample = min(stream.n_requests, args.ref_sample)
     s = stream.slice(0, n_sample)
+    if args.gpus > 1:       # the arm it stands beside: the sharded C2 x N workload
+        per, users = sharded_shape(args.config, args.gpus)
+        cfg = config_sharded(args.gpus, users, per)
+    else:
+        cfg = config_n1(desc, stream.n_requests, stream.n_blocks(), stream.n_tokens)
     times = []
     for step in range(args.warmup + args.steps):
         o = Oracle(16, SEED, 2)
@@ -589,8 +622,7 @@ def run_reference(args):
             "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "blocks_per_s": s.n_blocks() * args.steps / tot,
-            "config": {"workload": desc, "policy": "solidarity",
-                       "sample": f"first {n_sample} requests per step"},
+            "config": cfg,
             "cpu_baseline": {"value": v, "unit": "requests/s", "cores": 1, "kind": "oracle",
                              "sample": f"first {n_sample} requests ({s.n_blocks()} blocks) of the "
                                        f"workload per step, sequential oracle, 1 thread"},
@@ -613,8 +645,7 @@ def run_sharded(args, world, rank, local):
                                             TorchExchange, run_protocol, run_protocol_device)
     from workloads import c2_shared_prompt
 
-    per = 100_000 if args.config == "c2" else 10_000
-    users = (1000 if args.config == "c2" else 100) * world
+    per, users = sharded_shape(args.config, world)
     lo, hi = rank * per, (rank + 1) * per
     s = c2_shared_prompt(users=users, reqs_per_user=100, lo=lo, hi=hi, seed=SEED + 2)
     nblk = s.n_blocks()
@@ -772,12 +803,8 @@ def run_sharded(args, world, rank, local):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic",
             "blocks_per_s": nblk * world * args.steps / (tot_ms / 1e3),
-            "config": {"workload": f"c2_shared_prompt x{world}: {users} users x 100 requests, "
-                                   f"2000-token prompts, {per} requests per GPU",
-                       "policy": "solidarity", "parallelism": f"key-hash-sharded index over "
-                       f"{world} GPUs, record exchange per resolver round",
-                       "exchange": xname,
-                       "l2": "inputs larger than L2", "restore": "index reset before each step"},
+            "config": config_sharded(world, users, per),
+            "exchange": xname,
             "roofline": {"bound": "hbm", "kernel": "whole sharded step (per GPU)",
                          "achieved": alg / world / (tot_ms / args.steps / 1e3) / 1e9,
                          "peak": peak, "unit": "GB/s",
@@ -1085,14 +1112,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic",
             "blocks_per_s": nblk * world * args.steps / (tot_ms / 1000.0),
-            "config": {"workload": desc, "policy": "solidarity", "batch_requests": N,
-                       "blocks_per_batch": nblk, "tokens_per_batch": stream_np.n_tokens,
-                       "parallelism": f"{world} independent tenant partitions (weak)",
-                       "l2": "inputs (800 MB tokens) larger than L2 (126 MB); no flush",
-                       "restore": "index reset to empty before every step, outside the events "
-                                  "(stream-ordered between consecutive steps)",
-                       "submission": "solid_admit_batch pipelined: step k+1 enqueued before "
-                                     "step k's status is collected"},
+            "config": config_n1(desc, N, nblk, stream_np.n_tokens),
             "roofline": roofline,
             "resolver_roofline": resolver_roofline,
             "cpu_baseline": cpu,
