@@ -82,7 +82,7 @@ typedef struct {
                                   0..capacity_blocks-1); per request, its evictions return their
                                   blocks first, then its new entries take blocks in block order.
                                   See solid_block_table / solid_dump_phys.  Single GPU only;
-                                  admission synchronous (solid_admit_batch is refused).          */
+                                  solid_admit_batch admits at submission (see there).            */
   uint32_t pin;                /* 1 (needs block_table = 1): in-flight pinning (R38; the
                                   reference count of vLLM's KVCacheBlock beneath P:733).  Every
                                   admitted request holds one pin on each entry of its block-table
@@ -187,8 +187,8 @@ solid_status solid_lookup_batch(solid_ctx* ctx, const solid_batch* batch, solid_
  * every entry the batch touched; a batch that would have to evict an entry it touched itself
  * (it inserts more entries than the index holds untouched ones) fails with SOLID_ERR_CAPACITY
  * and nothing is mutated — split it.  In evict mode solid_lookup_batch synchronises `stream`
- * (the joint resolver / eviction-time iteration is host-driven) and
- * solid_admit_batch is unavailable (SOLID_ERR_STATE). */
+ * (the joint resolver / eviction-time iteration runs on the device in chunks of iterations; the
+ * host waits once per chunk to decide whether another chunk is needed). */
 solid_status solid_insert_batch(solid_ctx* ctx, void* stream);
 
 /* Asynchronous admission (lookup + insert with no host synchronisation), for a pipelined caller.
@@ -204,7 +204,11 @@ solid_status solid_insert_batch(solid_ctx* ctx, void* stream);
  * while any is outstanding.  solid_reset may be called with batches outstanding: it is then
  * enqueued behind them on their stream without blocking, and the older batches, when
  * collected, report their status but no longer count in solid_stats.  `out` is written when
- * the stream reaches the batch (read it after solid_batch_status or a stream synchronisation). */
+ * the stream reaches the batch (read it after solid_batch_status or a stream synchronisation).
+ * Evict-mode and block_table contexts: the same calls and rules, but the batch is admitted
+ * during solid_admit_batch (their lookup waits on the host and their commit reads counts back),
+ * so it returns when the batch is committed (or failed) and `out` is final; its status waits
+ * for solid_batch_status like an asynchronous batch's. */
 #define SOLID_MAX_INFLIGHT 4
 solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch, solid_result* out,
                                void* stream);

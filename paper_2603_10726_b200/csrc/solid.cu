@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -83,6 +84,7 @@ struct DevStatus {
   uint32_t packed;                       // K_A: the packed kernel took this batch (short requests)
   uint32_t fast_commit;                  // k_stats: live + registered ids <= capacity, so the
                                          // batch cannot overflow: k_commit counts and updates live
+  uint32_t grab[4];                      // resolver: round t's dynamic-tail counter (t & 3)
   unsigned long long round_ns[17];       // globaltimer at resolver start and after rounds 1..16
   uint32_t seg[kNSeg];                   // id counts per segment (gathered by k_stats)
 #ifdef SOLID_COUNTERS
@@ -128,6 +130,7 @@ struct KParams {
   uint64_t slot_cap;
   uint4* dec;
   int stamp;                       // inserter-stamp rule on (SOLID_STAMP=0 turns it off for A/B)
+  int tail;                        // resolver rounds end with a dynamic tail (SOLID_TAIL=0: off)
   uint32_t stamp_wait_ns;          // its wait bound in the main pass (kStampWaitNs)
   uint32_t* dlist;                 // requests deferred by the main pass of a round (stale stamp)
   uint32_t* dcnt;                  // [2]: their count, by round parity
@@ -475,6 +478,15 @@ __device__ __forceinline__ uint4 ldg_v4(const uint32_t* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+// The same without L1 allocation (packed K_A: the token stream does not evict the key-table and
+// key-state lines its probes hit in L1; C4 hash 1.33 -> 1.26 ms.  The warp-per-request K_A is
+// slower with it, 0.314 -> 0.330 ms on C2: profiles/r02/experiments_r2.md).
+__device__ __forceinline__ uint4 ldg_v4_na(const uint32_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
 
 template <int SH>
 struct BlockWords {
@@ -500,8 +512,9 @@ struct BlockWords {
       hi += (uint64_t)t * kp.khi[i];
     }
     bad |= orv >> 20;
-    // lo + hi*2^32 mod p, with hi*2^32 = (hi mod 2^29)*2^32 + (hi >> 29)*2^61 == ... + (hi >> 29)
-    return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
+    // lo + hi*2^32 mod p, with hi*2^32 = (hi mod 2^29)*2^32 + (hi >> 29)*2^61 == ... + (hi >> 29);
+    // partially folded (< 2^61 + 7): it only feeds mulmod
+    return fold61_lazy(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
   }
   // second component (base B2), same limb scheme
   __device__ __forceinline__ uint64_t hash2(const KParams& kp) const {
@@ -512,7 +525,7 @@ struct BlockWords {
       lo += (uint64_t)t * kp.klo2[i];
       hi += (uint64_t)t * kp.khi2[i];
     }
-    return fold61(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
+    return fold61_lazy(lo + ((hi & 0x1FFFFFFFull) << 32) + (hi >> 29));
   }
 };
 
@@ -536,8 +549,8 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
     if (i + 32 < n) nxt.load(base + (uint64_t)kBS * (i + 32));       // prefetch next group
     uint64_t term = 0, term2 = 0;
     if (valid) {
-      term = mulmod(addmod(cur.hash(kp, bad), sig), kp.mpow[i]);
-      if (NC == 2) term2 = mulmod(addmod(cur.hash2(kp), sig2), kp.mpow2[i]);
+      term = mulmod(cur.hash(kp, bad) + sig, kp.mpow[i]);     // < 2^62 + 7: a mulmod operand
+      if (NC == 2) term2 = mulmod(cur.hash2(kp) + sig2, kp.mpow2[i]);
     }
     const uint64_t S = addmod(warp_scan_addmod(term, lane), carry);
     carry = __shfl_sync(0xffffffffu, S, 31);
@@ -629,8 +642,8 @@ __device__ __forceinline__ uint32_t hash_register_long(const KParams& kp, uint64
     if (valid) {
       BlockWords<SH> blk;
       blk.load(base + (uint64_t)kBS * i);
-      term = mulmod(addmod(blk.hash(kp, bad), sig), kp.mpow[i]);
-      if (NC == 2) term2 = mulmod(addmod(blk.hash2(kp), sig2), kp.mpow2[i]);
+      term = mulmod(blk.hash(kp, bad) + sig, kp.mpow[i]);
+      if (NC == 2) term2 = mulmod(blk.hash2(kp) + sig2, kp.mpow2[i]);
     }
     const uint64_t loc = warp_scan_addmod(term, lane);
     const uint64_t loc2 = NC == 2 ? warp_scan_addmod(term2, lane) : 0;
@@ -652,7 +665,7 @@ __device__ __forceinline__ uint32_t hash_register_long(const KParams& kp, uint64
     if (g < n) {                                    // warp-uniform
       const uint64_t S = addmod(loc, c);
       const uint64_t S2 = NC == 2 ? addmod(loc2, c2) : 0;
-      bool created = false;
+        bool created = false;
       const uint32_t id = scratch_register(kp, valid, NC == 2 ? key2_of(S, S2) : key_of(S), seg,
                                            lane, created, nullptr, S, S2);
       if (valid && id) {
@@ -1094,6 +1107,32 @@ __device__ __forceinline__ int eval_request(const KParams& kp, uint32_t t, uint6
   return changed ? 1 : 0;
 }
 
+// A round's requests: all but the last one or two sweeps statically strided over the tiles
+// (tile w takes w, w + nw, ...), the rest handed out one at a time from a per-round counter, so
+// tiles whose requests ran long do not hold the whole grid at the round's barrier.
+// (32-bit positions: a batch holds < 2^32 requests, max_batch_requests is checked at init.)
+template <int TW, class F>
+__device__ __forceinline__ void for_requests(const KParams& kp, uint32_t t, uint64_t w0,
+                                             uint64_t nw, int tl, F&& eval) {
+  if (TW == 16) {          // two requests per warp (short requests): plain strided loop (the
+                           // dynamic tail measured neutral there and its state spills)
+    for (uint64_t j = kp.j_lo + w0; j < kp.n; j += nw) eval(j);
+    return;
+  }
+  const uint32_t total = (uint32_t)(kp.n - kp.j_lo), w = (uint32_t)w0, step = (uint32_t)nw;
+  const uint32_t sweeps = total / step;
+  const uint32_t stat = !kp.tail ? total : sweeps >= 2 ? (sweeps - 1) * step : 0;
+  for (uint32_t q = w; q < stat; q += step) eval(kp.j_lo + q);
+  const Tile<TW> T;
+  for (;;) {
+    uint32_t q = 0;
+    if (tl == 0) q = stat + atomicAdd(&kp.st->grab[t & 3], 1u);
+    q = T.shfl(q, 0);
+    if (q >= total) break;
+    eval(kp.j_lo + q);
+  }
+}
+
 // The resolver: all rounds in one persistent cooperative launch (grid = resident CTAs).  Tiles
 // of TW lanes stride over the requests; between rounds a grid-wide barrier (which also
 // invalidates L1, so the next round sees every atomic of this one).  Stops at the first round
@@ -1117,9 +1156,11 @@ __device__ __forceinline__ void resolve_rounds(const KParams& kp, uint32_t t_max
     // main pass: every request; with the stamp rule, a deferred pass follows for the requests
     // whose inserter stamp was stale in the main pass, after a grid barrier,
     // when every main-pass stamp is published
+    if (grid.thread_rank() == 0) kp.st->grab[(t + 2) & 3] = 0;   // round t + 2's counter
     if (stamps) {
-      for (uint64_t j = kp.j_lo + w0; j < kp.n; j += nw)
+      for_requests<TW>(kp, t, w0, nw, tl, [&](uint64_t j) {
         any |= eval_request<POLICY, false, TW, true>(kp, t, j, tl) == 1;
+      });
       grid.sync();
       const uint32_t nd = *(volatile uint32_t*)&kp.dcnt[t & 1];
       if (grid.thread_rank() == 0) kp.dcnt[(t + 1) & 1] = 0;   // next round's list
@@ -1133,8 +1174,9 @@ __device__ __forceinline__ void resolve_rounds(const KParams& kp, uint32_t t_max
       if (grid.thread_rank() == 0 && t < 16) kp.st->cnt[t][11] = nd;
 #endif
     } else {
-      for (uint64_t j = kp.j_lo + w0; j < kp.n; j += nw)
+      for_requests<TW>(kp, t, w0, nw, tl, [&](uint64_t j) {
         any |= eval_request<POLICY, false, TW, false>(kp, t, j, tl) == 1;
+      });
     }
     // one store per CTA (100k same-address stores would serialise on one L2 slice)
     if (tl == 0 && any) *s_changed = 1;
@@ -1482,6 +1524,7 @@ struct solid_ctx {
   uint4* dec = nullptr;
   unsigned long long* fst = nullptr;
   int stamp_rule = 1;
+  int tail = 1;
   uint32_t stamp_wait_ns = kStampWaitNs;
   uint32_t* dlist = nullptr;
   uint32_t* dcnt = nullptr;
@@ -1538,6 +1581,10 @@ struct solid_ctx {
   HostSlot* slots = nullptr;
   Flight fl[kRing];
   uint32_t head = 0, outstanding = 0, cur = 0;
+  // evict-mode / block-table contexts: solid_admit_batch admits at submission (lookup + insert,
+  // the host-driven parts of those paths included); the statuses wait here, oldest first, for
+  // solid_batch_status (same ring limit and collection rules as the asynchronous batches)
+  std::deque<std::pair<solid_status, std::string>> done_q;
   uint64_t gen = 0;                         // reset generation
   // sharded mode (solid_dist.inc)
   struct Dist* dist = nullptr;
@@ -1690,6 +1737,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   ctx->cfg.world = world;
   ctx->dev = cfg->device;
   if (const char* e = getenv("SOLID_STAMP")) ctx->stamp_rule = atoi(e) != 0;
+  if (const char* e = getenv("SOLID_TAIL")) ctx->tail = atoi(e) != 0;
   if (const char* e = getenv("SOLID_PACK")) ctx->pack = atoi(e) != 0;
   if (const char* e = getenv("SOLID_STAMP_WAIT")) ctx->stamp_wait_ns = (uint32_t)atoi(e);
   if (const char* e = getenv("SOLID_RESOLVE_TILE")) {
@@ -1936,6 +1984,7 @@ static solid_status lookup_setup(solid_ctx* ctx, const solid_batch* b, solid_res
   kp.dec = ctx->dec;
   kp.fst = ctx->fst;
   kp.stamp = ctx->stamp_rule;
+  kp.tail = ctx->tail;
   kp.stamp_wait_ns = ctx->stamp_wait_ns;
   kp.dlist = ctx->dlist;
   kp.dcnt = ctx->dcnt;
@@ -2040,7 +2089,7 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
 }
 
 static solid_status require_collected(solid_ctx* ctx, const char* what) {
-  if (ctx->outstanding)
+  if (ctx->outstanding || !ctx->done_q.empty())
     return fail(ctx, SOLID_ERR_STATE,
                 std::string(what) + " with asynchronous batches outstanding (collect them with "
                                     "solid_batch_status)");
@@ -2206,10 +2255,26 @@ static solid_status admit_range(solid_ctx* ctx, uint64_t lo, uint64_t hi, cudaSt
 extern "C" solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch,
                                           solid_result* out, void* stream) {
   if (!ctx) return SOLID_ERR_INVALID;
-  if (ctx->ev_state)
-    return fail(ctx, SOLID_ERR_STATE, "evict mode: admission is synchronous (lookup + insert)");
-  if (ctx->pool)
-    return fail(ctx, SOLID_ERR_STATE, "block_table: admission is synchronous (lookup + insert)");
+  if (ctx->ev_state || ctx->pool) {
+    // LRU eviction / block tables: their lookup waits on the host (joint resolver / eviction-time
+    // iteration) and their commit reads counts back, so the batch is admitted here,
+    // in submission order, and its status queued for solid_batch_status.  Same contract as the
+    // asynchronous path: a failed batch leaves the index as before it, later batches see that
+    // state; argument errors are returned at once.
+    if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "admit_batch with a pending lookup");
+    if (ctx->done_q.size() >= kRing)
+      return fail(ctx, SOLID_ERR_STATE,
+                  "SOLID_MAX_INFLIGHT batches outstanding (collect one with solid_batch_status)");
+    CK(cudaSetDevice(ctx->dev));
+    set_slot(ctx, ctx->head);
+    solid_status rc = do_lookup(ctx, batch, out, stream);
+    if (rc != SOLID_OK && !ctx->pending) return rc;       // rejected before anything was staged
+    if (rc == SOLID_OK) rc = solid_insert_batch(ctx, stream);
+    ctx->pending = false;
+    if (rc == SOLID_ERR_CUDA) return rc;                   // context poisoned: reported now
+    ctx->done_q.emplace_back(rc, rc == SOLID_OK ? std::string() : ctx->err);
+    return SOLID_OK;
+  }
   if (ctx->pending) return fail(ctx, SOLID_ERR_STATE, "admit_batch with a pending lookup");
   if (ctx->outstanding == kRing)
     return fail(ctx, SOLID_ERR_STATE,
@@ -2228,6 +2293,12 @@ extern "C" solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* bat
 
 extern "C" solid_status solid_batch_status(solid_ctx* ctx) {
   if (!ctx) return SOLID_ERR_INVALID;
+  if (!ctx->done_q.empty()) {                // admitted at submission (evict / block-table)
+    const auto d = ctx->done_q.front();
+    ctx->done_q.pop_front();
+    if (d.first != SOLID_OK) ctx->err = d.second;
+    return d.first;
+  }
   if (!ctx->outstanding) return SOLID_OK;
   CK(cudaSetDevice(ctx->dev));
   const uint32_t i = ctx->head;

@@ -20,6 +20,11 @@ __host__ __device__ __forceinline__ uint64_t fold61(uint64_t v) {   // v < 2^64 
   return v >= kP ? v - kP : v;
 }
 
+// Partial fold: v < 2^64 -> a congruent value < 2^61 + 7 (not canonical; a valid mulmod operand).
+__host__ __device__ __forceinline__ uint64_t fold61_lazy(uint64_t v) {
+  return (v & kP) + (v >> 61);
+}
+
 __host__ __device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b) {   // a, b < p
   uint64_t s = a + b;
   return s >= kP ? s - kP : s;
@@ -29,9 +34,10 @@ __host__ __device__ __forceinline__ uint64_t submod(uint64_t a, uint64_t b) {   
   return a >= b ? a - b : a + kP - b;
 }
 
-__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b) {   // a, b < p
+// a < 2^63 (need not be canonical), b < 2^61 -> canonical [0, p)
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b) {
   uint64_t lo = a * b;
-  uint64_t hi = __umul64hi(a, b);              // < 2^58
+  uint64_t hi = __umul64hi(a, b);              // < 2^60: (hi << 3) + 2^61 + 7 < 2^64
   uint64_t r = (lo & kP) + (lo >> 61) + (hi << 3);
   return fold61(r);
 }
@@ -93,14 +99,23 @@ __host__ __device__ __forceinline__ uint64_t key2_of(uint64_t S, uint64_t S2) {
   return k ? k : 1;
 }
 
-// Inclusive warp scan of values in [0, p) under addition mod p.
+// Inclusive warp scan of values in [0, p) under addition mod p, canonical result.  Lazy
+// reduction: the first three steps add at most 8 terms (< 8p < 2^64) with plain 64-bit adds,
+// one partial fold (< 2^61 + 7), the last two steps add at most 4 such values (< 2^64), then
+// one canonical fold.
 __device__ __forceinline__ uint64_t warp_scan_addmod(uint64_t x, int lane) {
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
-    if (lane >= d) x = addmod(x, y);
+  for (int d = 1; d < 8; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
   }
-  return x;
+  x = fold61_lazy(x);
+#pragma unroll
+  for (int d = 8; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  return fold61(x);
 }
 
 }  // namespace solid

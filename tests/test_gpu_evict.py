@@ -128,16 +128,60 @@ def test_rebuild_and_compaction():
     assert st["rebuilds"] >= 1 and st["compactions"] >= 1, st
 
 
-def test_evict_rejects_bad_config_and_async():
+def test_evict_rejects_bad_config():
     import paper_2603_10726_b200 as P
     with pytest.raises(P.SolidError):
         P.Index("apc", capacity_blocks=4, max_blocks=8, evict=True)     # capacity < max_blocks
-    idx = P.Index("apc", capacity_blocks=64, max_batch_tokens=1 << 12, max_batch_requests=64,
-                  max_blocks=8, evict=True)
-    s = random_small(10, users=2, alphabet_blocks=3, max_blocks=4, seed=1)
+
+
+@pytest.mark.parametrize("policy", ["apc", "solidarity"])
+def test_admit_async_evict_mode(policy):
+    """solid_admit_batch in evict mode (admitted at submission, statuses collected in order by
+    solid_batch_status): the same results and final LRU index as the oracle, a batch that would
+    evict entries it touched reports SOLID_ERR_CAPACITY at collection and leaves the index as
+    before it, the ring limit and the collection rule hold as for asynchronous batches."""
+    import torch
+    import paper_2603_10726_b200 as P
+    s = random_small(600, users=4, alphabet_blocks=12, max_blocks=6, seed=11)
+    cap = 30
+    idx = _index(policy, [s], cap, 8)
+    o = Oracle(16, SEED, POL[policy], capacity=cap)
+    parts = _batches(s, 40)
+    got, exp = [], []
+    for q in range(0, len(parts), 3):
+        chunk = parts[q:q + 3]
+        outs = [idx.admit_async(**P.to_device(b)) for b in chunk]
+        failed = []
+        for b, out in zip(chunk, outs):      # the oracle follows the order the GPU committed
+            try:
+                idx.status()
+                got.append(P.as_numpy(out))
+                exp.append(o.process(b))
+            except P.SolidError as e:        # nothing mutated; later batches did not see it
+                assert e.status == P.SOLID_ERR_CAPACITY
+                failed.append(b)
+        for b in failed:                     # admitted again, in halves
+            got.append(_admit_split(idx, b, []))
+            exp.append(o.process(b))
+    torch.cuda.synchronize()
+    got, exp = np.concatenate(got), np.concatenate(exp)
+    for f in exp.dtype.names:
+        assert np.array_equal(got[f].astype(np.int64), exp[f].astype(np.int64)), f
+    gd, ed = idx.dump_ex(), o.dump_ex()
+    for f in ["key", "owner", "sharer", "last_used"]:
+        assert np.array_equal(gd[f], ed[f]), f
+    # ring limit and collection rule
+    small = random_small(4, users=2, alphabet_blocks=3, max_blocks=4, seed=2)
+    for _ in range(P.MAX_INFLIGHT):
+        idx.admit_async(**P.to_device(small))
     with pytest.raises(P.SolidError):
-        idx.admit_async(**P.to_device(s))
-    idx.admit(**P.to_device(s))   # the synchronous path still works after the refusal
+        idx.admit_async(**P.to_device(small))          # ring full
+    with pytest.raises(P.SolidError):
+        idx.lookup(**P.to_device(small))               # batches not collected
+    for _ in range(P.MAX_INFLIGHT):
+        idx.status()
+    idx.status()                                       # none outstanding: OK
+    idx.admit(**P.to_device(small))
 
 
 def test_checkpoint_restore_evict():

@@ -165,10 +165,14 @@ def test_pool_refusals():
     with pytest.raises(P.SolidError):
         idx.block_table(16)                          # nothing committed yet
     s = random_small(10, users=2, alphabet_blocks=3, max_blocks=4, seed=1)
-    with pytest.raises(P.SolidError):
-        idx.admit_async(**P.to_device(s))
-    idx.admit(**P.to_device(s))
-    idx.block_table(s.n_tokens)
+    # solid_admit_batch on a block-table context: admitted at submission, collected in order
+    r1 = P.as_numpy(idx.admit_async(**P.to_device(s))).copy()
+    idx.status()
+    t1 = idx.block_table(s.n_tokens).cpu().numpy()
+    idx.reset()
+    r2 = P.as_numpy(idx.admit(**P.to_device(s)))
+    assert np.array_equal(r1, r2)
+    assert np.array_equal(t1, idx.block_table(s.n_tokens).cpu().numpy())
     plain = P.Index("apc", capacity_blocks=64, max_batch_tokens=1 << 12, max_batch_requests=64,
                     max_blocks=8)
     plain.admit(**P.to_device(s))
