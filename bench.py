@@ -1003,7 +1003,8 @@ def main():
     if not args.profile and args.e2e_steps > 0:
         pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
         ht, ho, hu = pin(stream_np.tokens), pin(stream_np.offsets), pin(stream_np.users)
-        hout = np.zeros(N, dtype=P.RESULT_DTYPE)
+        hout = (torch.zeros(N * P.RESULT_DTYPE.itemsize, dtype=torch.uint8).pin_memory().numpy()
+                .view(P.RESULT_DTYPE))                   # pinned: the result copy is a DMA
         idx.reset()
         idx.admit_host(ht, ho, hu, None, out=hout)
         e2e_t = 0.0

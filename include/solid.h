@@ -215,7 +215,11 @@ solid_status solid_admit_batch(solid_ctx* ctx, const solid_batch* batch, solid_r
 solid_status solid_batch_status(solid_ctx* ctx);
 
 /* lookup + insert with HOST buffers: copies the batch to the device, admits it, copies the
- * results back to out_host (HOST memory) and synchronises `stream`. */
+ * results back to out_host (HOST memory; page-locked memory makes that copy a DMA) and
+ * synchronises `stream`.  Large batches are copied in 4 pieces (the last one half the size of
+ * the others) on a second stream, each hashed as soon as it has arrived; the commit and the
+ * result copy share one host wait.  On failure the index is untouched and out_host is
+ * unspecified. */
 solid_status solid_admit_host(solid_ctx* ctx, const solid_batch* host_batch,
                               solid_result* out_host, void* stream);
 

@@ -488,11 +488,27 @@ __device__ __forceinline__ uint4 ldg_v4_na(const uint32_t* p) {
   return r;
 }
 
-template <int SH>
+// 32-byte loads (LDG.E.256) of a 32-byte-aligned block: two per block, each covering whole
+// 32-byte sectors.
+__device__ __forceinline__ void ldg_v8(const uint32_t* p, uint32_t* r) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+
+// SH: the request's token offset mod 4 (16-byte loads of the aligned window); V8 (SH = 0 and
+// the request 32-byte aligned): two 32-byte loads per block.
+template <int SH, bool V8 = false>
 struct BlockWords {
   static constexpr int W = SH ? 20 : 16;
   uint32_t w[W];
   __device__ __forceinline__ void load(const uint32_t* p) {
+    if (V8) {
+      ldg_v8(p, w);
+      ldg_v8(p + 8, w + 8);
+      return;
+    }
     const uint32_t* a = p - SH;
 #pragma unroll
     for (int q = 0; q < W / 4; ++q) {
@@ -529,7 +545,7 @@ struct BlockWords {
   }
 };
 
-template <int POLICY, int SH, int NC>
+template <int POLICY, int SH, int NC, bool V8 = false>
 __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uint64_t j, int lane,
                                                           const uint32_t* base, uint32_t n,
                                                           uint64_t blk0, uint32_t u,
@@ -541,7 +557,7 @@ __device__ __forceinline__ uint32_t hash_register_request(const KParams& kp, uin
       ((unsigned long long)tag_of(kp.epoch, 0) << 32) | (unsigned long long)(kp.seq_base + j + 1);
   uint64_t carry = 0, carry2 = 0;
   uint32_t bad = 0;
-  BlockWords<SH> cur, nxt;
+  BlockWords<SH, V8> cur, nxt;
   if ((uint32_t)lane < n) cur.load(base + (uint64_t)kBS * lane);
   for (uint32_t g = 0; g < n; g += 32) {
     const uint32_t i = g + lane;
@@ -609,7 +625,11 @@ __global__ void __launch_bounds__(256, 4) k_hash_register(KParams kp, uint64_t j
   const uint32_t* base = kp.tokens + o0;
   uint32_t bad;
   switch (((uintptr_t)base >> 2) & 3) {
-    case 0: bad = hash_register_request<POLICY, 0, NC>(kp, j, lane, base, n, blk0, u, seg); break;
+    case 0:
+      bad = ((uintptr_t)base & 31)
+                ? hash_register_request<POLICY, 0, NC>(kp, j, lane, base, n, blk0, u, seg)
+                : hash_register_request<POLICY, 0, NC, true>(kp, j, lane, base, n, blk0, u, seg);
+      break;
     case 1: bad = hash_register_request<POLICY, 1, NC>(kp, j, lane, base, n, blk0, u, seg); break;
     case 2: bad = hash_register_request<POLICY, 2, NC>(kp, j, lane, base, n, blk0, u, seg); break;
     default: bad = hash_register_request<POLICY, 3, NC>(kp, j, lane, base, n, blk0, u, seg); break;
@@ -1492,6 +1512,7 @@ using namespace solid;
 
 constexpr uint32_t kRing = SOLID_MAX_INFLIGHT;   // asynchronous batches in flight per context
 constexpr uint32_t kHostChunks = 4;              // host admission: sub-batches of a large batch
+constexpr uint32_t kHostChunksMax = 16;          // (SOLID_HOST_CHUNKS, A/B only)
 struct HostSlot {               // pinned host mirror of one batch's status
   DevStatus st;
 };
@@ -1565,7 +1586,8 @@ struct solid_ctx {
   uint32_t* h_tokens = nullptr;
   uint16_t* h_tokens16 = nullptr;
   cudaStream_t s_copy = nullptr;               // host admission: token copies of later chunks
-  cudaEvent_t ev_chunk[kHostChunks + 1] = {};
+  cudaEvent_t ev_chunk[kHostChunksMax + 1] = {};
+  uint32_t host_chunks = kHostChunks;
   uint64_t* h_offsets = nullptr;
   uint32_t* h_users = nullptr;
   uint8_t* h_enforce = nullptr;
@@ -1738,6 +1760,10 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   ctx->dev = cfg->device;
   if (const char* e = getenv("SOLID_STAMP")) ctx->stamp_rule = atoi(e) != 0;
   if (const char* e = getenv("SOLID_TAIL")) ctx->tail = atoi(e) != 0;
+  if (const char* e = getenv("SOLID_HOST_CHUNKS")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= (int)kHostChunksMax) ctx->host_chunks = (uint32_t)v;
+  }
   if (const char* e = getenv("SOLID_PACK")) ctx->pack = atoi(e) != 0;
   if (const char* e = getenv("SOLID_STAMP_WAIT")) ctx->stamp_wait_ns = (uint32_t)atoi(e);
   if (const char* e = getenv("SOLID_RESOLVE_TILE")) {
@@ -2200,15 +2226,16 @@ static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, boo
   return SOLID_OK;
 }
 
-extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
-  if (!ctx) return SOLID_ERR_INVALID;
-  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
-  if (!ctx->pending) return fail(ctx, SOLID_ERR_STATE, "insert_batch without a pending lookup");
-  cudaStream_t s = (cudaStream_t)stream;
-  CK(cudaSetDevice(ctx->dev));
-  if (ctx->ev_state) return evict_insert(ctx, s);
+static solid_status admit_range(solid_ctx* ctx, uint64_t lo, uint64_t hi, cudaStream_t s);
+
+// Commit of the pending lookup (not evict mode) and one host wait.  `d2h_bytes` > 0: the batch's
+// results are copied to host memory in the same wait (host admission; they are copied again
+// after a split), so a converged batch costs a single synchronisation.
+static solid_status insert_sync(solid_ctx* ctx, cudaStream_t s, void* d2h_dst,
+                                const void* d2h_src, size_t d2h_bytes) {
   solid_status rc = enqueue_commit(ctx, s);
   if (rc != SOLID_OK) return rc;
+  if (d2h_bytes) CK(cudaMemcpyAsync(d2h_dst, d2h_src, d2h_bytes, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   ctx->pending = false;
   const DevStatus& h = ctx->slots[ctx->cur].st;
@@ -2222,9 +2249,23 @@ extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
     rc = admit_range(ctx, lo, mid, s);
     if (rc == SOLID_OK) rc = admit_range(ctx, mid, hi, s);
     ctx->split_last = true;
+    if (rc == SOLID_OK && d2h_bytes) {
+      CK(cudaMemcpyAsync(d2h_dst, d2h_src, d2h_bytes, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
     return rc;
   }
   return finish_batch(ctx, ctx->cur, s, false);
+}
+
+extern "C" solid_status solid_insert_batch(solid_ctx* ctx, void* stream) {
+  if (!ctx) return SOLID_ERR_INVALID;
+  if (ctx->poisoned) return fail(ctx, SOLID_ERR_STATE, "context poisoned by an earlier failure");
+  if (!ctx->pending) return fail(ctx, SOLID_ERR_STATE, "insert_batch without a pending lookup");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(ctx->dev));
+  if (ctx->ev_state) return evict_insert(ctx, s);
+  return insert_sync(ctx, s, nullptr, nullptr, 0);
 }
 
 // Admit requests [lo, hi) of the pending batch's arrays as a batch of their own (a part of a
@@ -2369,19 +2410,26 @@ static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* to
   CK(cudaMemcpyAsync(ctx->h_offsets, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
   if (n) CK(cudaMemcpyAsync(ctx->h_users, users, n * 4, cudaMemcpyHostToDevice, s));
   if (n && enforce) CK(cudaMemcpyAsync(ctx->h_enforce, enforce, n, cudaMemcpyHostToDevice, s));
-  const uint32_t K = (T * (uint64_t)token_bytes >= (64ull << 20) && n >= 4 * kHostChunks &&
-                      !ctx->ev_state) ? kHostChunks : 1u;
+  const uint32_t HC = ctx->host_chunks;
+  const uint32_t K = (T * (uint64_t)token_bytes >= (64ull << 20) && n >= 4 * HC &&
+                      !ctx->ev_state) ? HC : 1u;
   if (K > 1 && !ctx->s_copy) {
     CK(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
     for (auto& e : ctx->ev_chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t sc = K > 1 ? ctx->s_copy : s;
   if (K > 1) {                       // the copy stream starts after the small copies were enqueued
-    CK(cudaEventRecord(ctx->ev_chunk[kHostChunks], s));
-    CK(cudaStreamWaitEvent(sc, ctx->ev_chunk[kHostChunks], 0));
+    CK(cudaEventRecord(ctx->ev_chunk[kHostChunksMax], s));
+    CK(cudaStreamWaitEvent(sc, ctx->ev_chunk[kHostChunksMax], 0));
   }
+  // chunk boundaries (requests): K - 1 equal chunks and a last one of half their size, so the
+  // hashing left after the last copy is short
+  auto cut = [&](uint32_t k) -> uint64_t {
+    if (k >= K) return n;
+    return K == 1 ? 0 : n * k * (2 * K - 1) / (2ull * K * (K - 1));
+  };
   for (uint32_t k = 0; k < K; ++k) {
-    const uint64_t a = offsets[n * k / K], b = offsets[n * (k + 1) / K];
+    const uint64_t a = offsets[cut(k)], b = offsets[cut(k + 1)];
     if (b > a)
       CK(cudaMemcpyAsync(token_bytes == 2 ? (void*)(ctx->h_tokens16 + a) : (void*)(ctx->h_tokens + a),
                          (const char*)tokens + a * token_bytes, (b - a) * token_bytes,
@@ -2404,7 +2452,7 @@ static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* to
   } else if (rc == SOLID_OK) {
     CK(cudaEventRecord(ctx->ev[0], s));
     for (uint32_t k = 0; k < K; ++k) {
-      const uint64_t lo = n * k / K, hi = n * (k + 1) / K;
+      const uint64_t lo = cut(k), hi = cut(k + 1);
       const uint64_t a = offsets[lo], b = offsets[hi];
       if (K > 1) CK(cudaStreamWaitEvent(s, ctx->ev_chunk[k], 0));
       if (token_bytes == 2 && b > a) {   // widen from an 8-aligned start (earlier ids: same values)
@@ -2418,10 +2466,17 @@ static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* to
     }
     rc = lookup_resolve(ctx, s);
   }
-  if (rc == SOLID_OK) rc = solid_insert_batch(ctx, stream);
+  if (rc == SOLID_OK) {
+    if (ctx->ev_state) {
+      rc = solid_insert_batch(ctx, stream);
+      if (rc == SOLID_OK && n)
+        CK(cudaMemcpyAsync(out_host, ctx->h_out, n * sizeof(solid_result), cudaMemcpyDeviceToHost, s));
+    } else {         // commit + result copy, one host wait (the results are unspecified on failure)
+      rc = insert_sync(ctx, s, out_host, ctx->h_out, n * sizeof(solid_result));
+    }
+  }
   if (K > 1) cudaStreamSynchronize(sc);       // no copy may outlive a failed call
   if (rc != SOLID_OK) return rc;
-  if (n) CK(cudaMemcpyAsync(out_host, ctx->h_out, n * sizeof(solid_result), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return SOLID_OK;
 }
