@@ -1176,14 +1176,23 @@ __device__ __forceinline__ void resolve_rounds(const KParams& kp, uint32_t t_max
     // main pass: every request; with the stamp rule, a deferred pass follows for the requests
     // whose inserter stamp was stale in the main pass, after a grid barrier,
     // when every main-pass stamp is published
-    if (grid.thread_rank() == 0) kp.st->grab[(t + 2) & 3] = 0;   // round t + 2's counter
+    if (grid.thread_rank() == 0) {
+      kp.st->grab[(t + 2) & 3] = 0;      // round t + 2's counter
+      kp.dcnt[(t + 1) & 1] = 0;          // round t + 1's deferred list (last read in round t - 1)
+    }
+    bool synced = false;                 // the round's closing barrier was already passed
     if (stamps) {
       for_requests<TW>(kp, t, w0, nw, tl, [&](uint64_t j) {
         any |= eval_request<POLICY, false, TW, true>(kp, t, j, tl) == 1;
       });
+      // the main pass's changes are published before the barrier: with nothing deferred it
+      // closes the round (one grid barrier per round instead of two)
+      if (tl == 0 && any) *s_changed = 1;
+      __syncthreads();
+      if (threadIdx.x == 0 && *s_changed) kp.st->changed[t] = kp.epoch;
       grid.sync();
       const uint32_t nd = *(volatile uint32_t*)&kp.dcnt[t & 1];
-      if (grid.thread_rank() == 0) kp.dcnt[(t + 1) & 1] = 0;   // next round's list
+      synced = nd == 0;
 #ifdef SOLID_COUNTERS
       const unsigned long long td0 = globaltimer_ns();
 #endif
@@ -1199,16 +1208,18 @@ __device__ __forceinline__ void resolve_rounds(const KParams& kp, uint32_t t_max
       });
     }
     // one store per CTA (100k same-address stores would serialise on one L2 slice)
-    if (tl == 0 && any) *s_changed = 1;
-    __syncthreads();
-    if (threadIdx.x == 0 && *s_changed) kp.st->changed[t] = kp.epoch;
+    if (!synced) {
+      if (tl == 0 && any) *s_changed = 1;
+      __syncthreads();
+      if (threadIdx.x == 0 && *s_changed) kp.st->changed[t] = kp.epoch;
+    }
     if (POLICY != SOLID_POLICY_SOLIDARITY) {         // exact in one pass
       if (grid.thread_rank() == 0) kp.st->conv = 1;
       return;
     }
     // grid.sync(): bar.sync + release/acquire at gpu scope; the acquire path also invalidates
     // L1 (CCTL.IVALL in SASS), so the next round's weak loads see every write of this one
-    grid.sync();
+    if (!synced) grid.sync();
     if (grid.thread_rank() == 0 && t <= 16) kp.st->round_ns[t] = globaltimer_ns();
     // one L2 read per CTA, broadcast through shared memory
     __shared__ uint32_t s_ch, s_er;
