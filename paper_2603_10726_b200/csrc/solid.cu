@@ -130,7 +130,7 @@ struct KParams {
   uint64_t slot_cap;
   uint4* dec;
   int stamp;                       // inserter-stamp rule on (SOLID_STAMP=0 turns it off for A/B)
-  int tail;                        // resolver rounds end with a dynamic tail (SOLID_TAIL=0: off)
+  int tail;                        // resolver: last sweeps handed out dynamically (SOLID_TAIL, 0: off)
   uint32_t stamp_wait_ns;          // its wait bound in the main pass (kStampWaitNs)
   uint32_t* dlist;                 // requests deferred by the main pass of a round (stale stamp)
   uint32_t* dcnt;                  // [2]: their count, by round parity
@@ -176,6 +176,7 @@ struct KParams {
   uint8_t* win_skip;               // k_window's skip flag per window index (0 at creation)
   uint32_t* win_dense;             // [rank] = window index + 1 (0 = no window key of that rank)
   uint32_t* ins_cnt;               // per request: entries it inserts (final round)
+  uint32_t* ins_scan;              // merged joint step: their inclusive prefix (resolver tail)
   uint32_t* lt;                    // per id: last request served it (final)
 };
 
@@ -1127,7 +1128,7 @@ __device__ __forceinline__ int eval_request(const KParams& kp, uint32_t t, uint6
   return changed ? 1 : 0;
 }
 
-// A round's requests: all but the last one or two sweeps statically strided over the tiles
+// A round's requests: all but the last `tail` sweeps (2) statically strided over the tiles
 // (tile w takes w, w + nw, ...), the rest handed out one at a time from a per-round counter, so
 // tiles whose requests ran long do not hold the whole grid at the round's barrier.
 // (32-bit positions: a batch holds < 2^32 requests, max_batch_requests is checked at init.)
@@ -1141,7 +1142,8 @@ __device__ __forceinline__ void for_requests(const KParams& kp, uint32_t t, uint
   }
   const uint32_t total = (uint32_t)(kp.n - kp.j_lo), w = (uint32_t)w0, step = (uint32_t)nw;
   const uint32_t sweeps = total / step;
-  const uint32_t stat = !kp.tail ? total : sweeps >= 2 ? (sweeps - 1) * step : 0;
+  const uint32_t dyn = (uint32_t)kp.tail;           // sweeps handed out dynamically (0: none)
+  const uint32_t stat = !dyn ? total : sweeps > dyn ? (sweeps - dyn) * step : 0;
   for (uint32_t q = w; q < stat; q += step) eval(kp.j_lo + q);
   const Tile<TW> T;
   for (;;) {
@@ -1556,7 +1558,7 @@ struct solid_ctx {
   uint4* dec = nullptr;
   unsigned long long* fst = nullptr;
   int stamp_rule = 1;
-  int tail = 1;
+  int tail = 2;                  // resolver: sweeps handed out dynamically per round (SOLID_TAIL)
   uint32_t stamp_wait_ns = kStampWaitNs;
   uint32_t* dlist = nullptr;
   uint32_t* dcnt = nullptr;
@@ -1770,7 +1772,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   ctx->cfg.world = world;
   ctx->dev = cfg->device;
   if (const char* e = getenv("SOLID_STAMP")) ctx->stamp_rule = atoi(e) != 0;
-  if (const char* e = getenv("SOLID_TAIL")) ctx->tail = atoi(e) != 0;
+  if (const char* e = getenv("SOLID_TAIL")) ctx->tail = std::max(0, atoi(e));
   if (const char* e = getenv("SOLID_HOST_CHUNKS")) {
     const int v = atoi(e);
     if (v >= 1 && v <= (int)kHostChunksMax) ctx->host_chunks = (uint32_t)v;
