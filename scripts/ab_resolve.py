@@ -82,7 +82,7 @@ def main():
                 same = "same" if all(np.array_equal(r[f], ref[f]) for f in r.dtype.names) else "DIFFERENT"
             print(f"{cfg} [{v}] ms {statistics.median(ms):.4f} hash {st['ms_hash']:.3f} "
                   f"resolve {st['ms_resolve']:.3f} commit {st['ms_commit']:.3f} rounds {rounds[-1]} "
-                  f"round_us {rus[-1]} {same}", flush=True)
+                  f"round_us {rus[-1]} ids {st['last_distinct_keys']} {same}", flush=True)
             del idx, o
             torch.cuda.empty_cache()
 
