@@ -734,33 +734,38 @@ __global__ void __launch_bounds__(256, 4) k_hash_register_long(KParams kp) {
 // K_A on stream s (single GPU and sharded paths), for requests [lo, hi) of the batch (host
 // admission hashes each sub-range as soon as its tokens have arrived).
 template <int NC>
-static void launch_hash_nc(const KParams& kp, unsigned grid, uint64_t lo, uint64_t hi,
+static void launch_hash_nc(const KParams& kp, unsigned grid, unsigned B, uint64_t lo, uint64_t hi,
                            cudaStream_t s) {
   const unsigned lg = 148 * 4;   // persistent CTAs for the long requests (none: they exit at once)
   switch (kp.policy) {
     case SOLID_POLICY_APC:
-      k_hash_register<SOLID_POLICY_APC, NC><<<grid, 256, 0, s>>>(kp, lo, hi);
+      k_hash_register<SOLID_POLICY_APC, NC><<<grid, B, 0, s>>>(kp, lo, hi);
       if (kp.long_q) k_hash_register_long<SOLID_POLICY_APC, NC><<<lg, 256, 0, s>>>(kp);
       break;
     case SOLID_POLICY_USER_ISOLATION:
-      k_hash_register<SOLID_POLICY_USER_ISOLATION, NC><<<grid, 256, 0, s>>>(kp, lo, hi);
+      k_hash_register<SOLID_POLICY_USER_ISOLATION, NC><<<grid, B, 0, s>>>(kp, lo, hi);
       if (kp.long_q) k_hash_register_long<SOLID_POLICY_USER_ISOLATION, NC><<<lg, 256, 0, s>>>(kp);
       break;
     default:
-      k_hash_register<SOLID_POLICY_SOLIDARITY, NC><<<grid, 256, 0, s>>>(kp, lo, hi);
+      k_hash_register<SOLID_POLICY_SOLIDARITY, NC><<<grid, B, 0, s>>>(kp, lo, hi);
       if (kp.long_q) k_hash_register_long<SOLID_POLICY_SOLIDARITY, NC><<<lg, 256, 0, s>>>(kp);
       break;
   }
 }
-static cudaError_t launch_hash(const KParams& kp, cudaStream_t s, uint64_t lo, uint64_t hi) {
+// K_A threads per CTA: 256 (8 requests per CTA), or 64 when the batch is expected to take the
+// warp-per-request path (a CTA releases its slot as soon as its 2 requests are done: C2 hash
+// 0.296 -> 0.282 ms, C3 1.36 -> 1.34; a batch that the packed K_A takes would pay for 4x more
+// CTAs that exit at once: C4 1.26 -> 1.46 ms) — profiles/r02/ka_block_ab.txt
+static cudaError_t launch_hash(const KParams& kp, cudaStream_t s, uint64_t lo, uint64_t hi,
+                               unsigned B = 256) {
   if (hi <= lo) return cudaSuccess;
-  const unsigned grid = (unsigned)(((hi - lo) * 32 + 255) / 256);
-  if (kp.nc == 2) launch_hash_nc<2>(kp, grid, lo, hi, s);
-  else launch_hash_nc<1>(kp, grid, lo, hi, s);
+  const unsigned grid = (unsigned)(((hi - lo) * 32 + B - 1) / B);
+  if (kp.nc == 2) launch_hash_nc<2>(kp, grid, B, lo, hi, s);
+  else launch_hash_nc<1>(kp, grid, B, lo, hi, s);
   return cudaGetLastError();
 }
-static cudaError_t launch_hash(const KParams& kp, cudaStream_t s) {
-  return launch_hash(kp, s, 0, kp.n);
+static cudaError_t launch_hash(const KParams& kp, cudaStream_t s, unsigned B = 256) {
+  return launch_hash(kp, s, 0, kp.n, B);
 }
 
 #include "solid_pack.inc"
@@ -2115,8 +2120,20 @@ static solid_status launch_hash_packed(solid_ctx* ctx, cudaStream_t s) {
   return SOLID_OK;
 }
 
+// K_A CTA size for this context's next batch: 64 unless the last collected batch took the
+// packed K_A (SOLID_KA_BLOCK = 64 / 128 / 256 fixes it)
+static unsigned ka_block(const solid_ctx* ctx) {
+  static const int fixed = [] {
+    const char* e = getenv("SOLID_KA_BLOCK");
+    const int v = e ? atoi(e) : 0;
+    return (v == 64 || v == 128 || v == 256) ? v : 0;
+  }();
+  if (fixed) return (unsigned)fixed;
+  return ctx->pack_hint ? 256u : 64u;
+}
+
 static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result* out,
-                             void* stream) {
+                              void* stream) {
   solid_status rc = lookup_setup(ctx, b, out, stream);
   if (rc != SOLID_OK) return rc;
   cudaStream_t s = (cudaStream_t)stream;
@@ -2138,7 +2155,7 @@ static solid_status do_lookup(solid_ctx* ctx, const solid_batch* b, solid_result
       if (rc != SOLID_OK) return rc;
       ctx->launches += 1;
     }
-    CK(launch_hash(ctx->kp, s));
+    CK(launch_hash(ctx->kp, s, ka_block(ctx)));
     ctx->kp.pack = 0;                    // later launches of this batch (splits) are per range
     ctx->launches += 1;
   }
@@ -2493,7 +2510,7 @@ static solid_status admit_host_common(solid_ctx* ctx, uint64_t n, const void* to
             ctx->h_tokens16 + a8, ctx->h_tokens + a8, b - a8);
         CK(cudaGetLastError());
       }
-      CK(launch_hash(ctx->kp, s, lo, hi));
+      CK(launch_hash(ctx->kp, s, lo, hi, ka_block(ctx)));
       ++ctx->launches;
     }
     rc = lookup_resolve(ctx, s);
