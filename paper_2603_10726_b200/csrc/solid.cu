@@ -1564,9 +1564,7 @@ struct solid_ctx {
   unsigned long long* fst = nullptr;
   int stamp_rule = 1;
   int tail = 2;                  // resolver: sweeps handed out dynamically per round (SOLID_TAIL)
-  unsigned commit_gx = 16;       // k_commit CTAs per id segment (SOLID_COMMIT_GX fixes it;
-  bool commit_gx_fixed = false;  // else chosen from the last batch's distinct keys)
-  uint64_t ids_hint = 0;
+  unsigned commit_gx = 16;       // k_commit CTAs per id segment (SOLID_COMMIT_GX)
   uint32_t stamp_wait_ns = kStampWaitNs;
   uint32_t* dlist = nullptr;
   uint32_t* dcnt = nullptr;
@@ -1783,10 +1781,7 @@ extern "C" solid_status solid_init(const solid_config* cfg, solid_ctx** out) {
   if (const char* e = getenv("SOLID_TAIL")) ctx->tail = std::max(0, atoi(e));
   if (const char* e = getenv("SOLID_COMMIT_GX")) {
     const int v = atoi(e);
-    if (v >= 1 && v <= 64) {
-      ctx->commit_gx = (unsigned)v;
-      ctx->commit_gx_fixed = true;
-    }
+    if (v >= 1 && v <= 64) ctx->commit_gx = (unsigned)v;
   }
   if (const char* e = getenv("SOLID_HOST_CHUNKS")) {
     const int v = atoi(e);
@@ -1965,15 +1960,11 @@ static solid_status launch_resolve(solid_ctx* ctx, cudaStream_t s) {
 }
 
 static void launch_commit(solid_ctx* c, int mode, cudaStream_t s) {
-  // CTAs per id segment from the last collected batch's distinct keys: a grid of about one
-  // wave for ~2 M ids (C2: 0.089 -> 0.073 ms), more CTAs for larger batches (C4 5.4 M ids: 8,
-  // C3 10 M: 16) (profiles/r02/commit_grid_ab.txt); SOLID_COMMIT_GX fixes it
-  unsigned gx = c->commit_gx;
-  if (!c->commit_gx_fixed) {
-    const uint64_t ids = c->ids_hint;
-    gx = ids == 0 ? 16u : ids <= 3000000 ? 6u : ids <= 7000000 ? 8u : 16u;
-  }
-  k_commit<<<dim3(gx, kNSeg), 256, 0, s>>>(c->kp, mode);   // 4 staged ids per thread
+  // 16 CTAs per id segment (SOLID_COMMIT_GX): fewer CTAs looked faster when the index is
+  // restored from a checkpoint before each batch (scripts/ab_resolve.py) but are slower in the
+  // bench, whose index is reset (C2 commit 0.079 ms with 16, 0.090-0.092 with 6 or 8,
+  // profiles/r02/commit_grid_bench_ab.txt)
+  k_commit<<<dim3(c->commit_gx, kNSeg), 256, 0, s>>>(c->kp, mode);   // 4 staged ids per thread
   if (mode == 1) k_live<<<1, kNSeg, 0, s>>>(c->st, c->live_dev, c->seg_new);
 }
 
@@ -2257,7 +2248,6 @@ static solid_status finish_batch(solid_ctx* ctx, uint32_t i, cudaStream_t s, boo
   for (int q = 0; q < kNSeg; ++q)
     distinct += std::min<uint32_t>(ctx->slots[i].st.seg[q], ctx->seg_cap);
   S.last_distinct_keys = (uint32_t)std::min<uint64_t>(distinct, 0xFFFFFFFFull);
-  ctx->ids_hint = distinct;            // sizes the next commit's grid (kept across solid_reset)
   S.last_shared_keys = (uint32_t)std::min<unsigned long long>(h.ids_after_hash, 0xFFFFFFFFull);
   S.last_kernel_launches = f.launches;
   S.last_requests = n;
