@@ -1133,7 +1133,7 @@ __device__ __forceinline__ int eval_request(const KParams& kp, uint32_t t, uint6
   return changed ? 1 : 0;
 }
 
-// A round's requests: all but the last `tail` sweeps (2) statically strided over the tiles
+// A round's requests: all but the last `tail` sweeps (1) statically strided over the tiles
 // (tile w takes w, w + nw, ...), the rest handed out one at a time from a per-round counter, so
 // tiles whose requests ran long do not hold the whole grid at the round's barrier.
 // (32-bit positions: a batch holds < 2^32 requests, max_batch_requests is checked at init.)
@@ -1563,7 +1563,7 @@ struct solid_ctx {
   uint4* dec = nullptr;
   unsigned long long* fst = nullptr;
   int stamp_rule = 1;
-  int tail = 2;                  // resolver: sweeps handed out dynamically per round (SOLID_TAIL)
+  int tail = 1;                  // resolver: sweeps handed out dynamically per round (SOLID_TAIL)
   unsigned commit_gx = 16;       // k_commit CTAs per id segment (SOLID_COMMIT_GX)
   uint32_t stamp_wait_ns = kStampWaitNs;
   uint32_t* dlist = nullptr;
