@@ -2117,7 +2117,7 @@ static unsigned ka_block(const solid_ctx* ctx) {
   static const int fixed = [] {
     const char* e = getenv("SOLID_KA_BLOCK");
     const int v = e ? atoi(e) : 0;
-    return (v == 64 || v == 128 || v == 256) ? v : 0;
+    return (v == 32 || v == 64 || v == 128 || v == 256) ? v : 0;
   }();
   if (fixed) return (unsigned)fixed;
   return ctx->pack_hint ? 256u : 64u;
